@@ -1,0 +1,896 @@
+// libsftgpu C ABI: plans, launch dispatch, workspace, host transfers, and the
+// C wrappers of the host precompute (fits / spec factories). See include/sftgpu.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/sftgpu.h"
+#include "aux_kernels.cuh"
+#include "host_fit.hpp"
+#include "scan_launch.cuh"
+
+namespace {
+
+using cd = std::complex<double>;
+thread_local std::string g_err;
+
+struct ApiError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& m) { throw ApiError{code, m}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(SFTGPU_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SFTGPU_OK;
+  } catch (const ApiError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const sftb::FitDegenerate& e) {
+    g_err = e.what();
+    return SFTGPU_EDEGENERATE;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return SFTGPU_EINVAL;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return SFTGPU_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SFTGPU_EINTERNAL;
+  }
+}
+
+void require_device() {
+  int count = 0;
+  const cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    fail(SFTGPU_ECUDA, "no CUDA device available (libsftgpu has no CPU fallback)");
+}
+
+// z^m for z = e^{-alpha - i omega} (m may be negative).
+cd zpow(double alpha, double omega, double m) {
+  const double mag = std::exp(-alpha * m);
+  const double ang = omega * m;
+  return cd(mag * std::cos(ang), -mag * std::sin(ang));
+}
+
+// One component sequence of the lowered transform: frequency + combine weights on
+// (c, s) as in the reference combine loops (wc * c + ws * s, complex weights).
+struct Order {
+  double omega;
+  cd wc, ws;
+};
+
+struct Lowered {
+  std::vector<Order> orders;
+  double alpha = 0.0;
+  double prefactor = 1.0;
+  bool complex_out = false;
+  int K = 1;
+};
+
+// Group of <= kMaxOrd orders executed by one kernel launch.
+struct Group {
+  int nord = 0;
+  sftk::ScanParams<float> pf{};
+  sftk::ScanParams<double> pd{};
+  void* d_tab = nullptr;
+  double2* d_tab_tile = nullptr;
+};
+
+}  // namespace
+
+struct sftgpu_plan {
+  int is_components = 0;
+  int precision = SFTGPU_DOUBLE;
+  int mode = sftk::kModeReal;
+  int conv = 0;  // GCT3/MCT3 direct convolution plan
+  long long n = 0, batch = 0, lo = 0, count = 0;
+  int K = 1, boundary = SFTGPU_BOUNDARY_CLAMP;
+  int L = 4, NT = 256;
+  long long TT = 1024, tiles_per_signal = 0, warm_tiles = 0, total_tiles = 0;
+  std::vector<Group> groups;
+  int max_nord = 1;
+  unsigned long long* d_ticket = nullptr;
+  unsigned long long* d_flags = nullptr;
+  double2* d_agg = nullptr;
+  double2* d_incl = nullptr;
+  unsigned long long ticket_base = 0;
+  unsigned int epoch = 0;
+  // direct-convolution plans
+  double2* d_taps = nullptr;
+  long long n_taps = 0, tap_lo = 0;
+  double2* d_conv_tmp = nullptr;
+  // host-transfer staging
+  void* d_x = nullptr;
+  void* d_out = nullptr;
+  size_t cap_x = 0, cap_out = 0;
+  int device = 0;
+
+  ~sftgpu_plan() {
+    for (Group& g : groups) {
+      cudaFree(g.d_tab);
+      cudaFree(g.d_tab_tile);
+    }
+    cudaFree(d_ticket);
+    cudaFree(d_flags);
+    cudaFree(d_agg);
+    cudaFree(d_incl);
+    cudaFree(d_taps);
+    cudaFree(d_conv_tmp);
+    cudaFree(d_x);
+    cudaFree(d_out);
+  }
+};
+
+namespace {
+
+size_t elem_size(int precision) { return precision == SFTGPU_SINGLE ? sizeof(float) : sizeof(double); }
+
+// ---------------------------------------------------------------- kernel dispatch
+template <typename T>
+void launch_scan(int L, int nord, int mode, const sftk::ScanParams<T>& p, long long grid, cudaStream_t s) {
+  if (nord < 1 || nord > sftk::kMaxOrd) fail(SFTGPU_EINTERNAL, "order group size out of range");
+  switch (mode) {
+    case sftk::kModeReal: sftk::launch_scan<T, sftk::kModeReal>(L, nord, p, grid, s); break;
+    case sftk::kModeComplex: sftk::launch_scan<T, sftk::kModeComplex>(L, nord, p, grid, s); break;
+    default: sftk::launch_scan<T, sftk::kModeComps>(L, nord, p, grid, s); break;
+  }
+}
+
+// ---------------------------------------------------------------- plan building
+template <typename T>
+void fill_consts(sftk::ScanParams<T>& P, const std::vector<Order>& ords, double alpha, double pref,
+                 int K, bool comps, double* Dr, double* Di) {
+  cd D(0.0, 0.0);
+  for (size_t i = 0; i < ords.size(); ++i) {
+    const double w = ords[i].omega;
+    const cd z = zpow(alpha, w, 1.0), c = zpow(alpha, w, 2.0 * K);
+    const cd a = zpow(alpha, w, -static_cast<double>(K)), b = zpow(alpha, w, static_cast<double>(K));
+    double k[4];
+    if (comps) {
+      k[0] = a.real();
+      k[1] = a.imag();
+      k[2] = b.real();
+      k[3] = b.imag();
+    } else {
+      const cd A = pref * (ords[i].wc + cd(0, 1) * ords[i].ws) * 0.5;
+      const cd B = pref * (ords[i].wc - cd(0, 1) * ords[i].ws) * 0.5;
+      const cd E = A * a, F = B * std::conj(a);
+      k[0] = E.real() + F.real();
+      k[1] = F.imag() - E.imag();
+      k[2] = E.imag() + F.imag();
+      k[3] = E.real() - F.real();
+      D += A * b + B * std::conj(b);
+    }
+    for (double v : k)
+      if (!std::isfinite(static_cast<double>(static_cast<T>(v))))
+        fail(SFTGPU_EINVAL, "attenuation alpha*K too large for the requested precision");
+    sftk::OrdConst<T>& o = P.oc[i];
+    o.zr = static_cast<T>(z.real());
+    o.zi = static_cast<T>(z.imag());
+    o.cr = static_cast<T>(c.real());
+    o.ci = static_cast<T>(c.imag());
+    o.k1 = static_cast<T>(k[0]);
+    o.k2 = static_cast<T>(k[1]);
+    o.k3 = static_cast<T>(k[2]);
+    o.k4 = static_cast<T>(k[3]);
+  }
+  *Dr = D.real();
+  *Di = D.imag();
+}
+
+template <typename T>
+void build_tables(Group& g, const std::vector<Order>& ords, double alpha, int L, int NT) {
+  using T2 = typename sftk::Vec2<T>::t;
+  const int NW = NT / 32;
+  const long long TT = static_cast<long long>(L) * NT;
+  std::vector<T2> tab(static_cast<size_t>(ords.size()) * sftk::kTabStride);
+  std::vector<double2> tt(static_cast<size_t>(ords.size()) * sftk::kTileTab);
+  auto put = [](T2& d, cd v) {
+    d.x = static_cast<T>(v.real());
+    d.y = static_cast<T>(v.imag());
+  };
+  for (size_t p = 0; p < ords.size(); ++p) {
+    const double w = ords[p].omega;
+    T2* t = &tab[p * sftk::kTabStride];
+    for (int lane = 0; lane < 32; ++lane) put(t[lane], zpow(alpha, w, static_cast<double>(L) * lane));
+    for (int k = 0; k < 5; ++k) put(t[32 + k], zpow(alpha, w, static_cast<double>(L) * (1 << k)));
+    for (int wi = 0; wi < NW; ++wi) put(t[40 + wi], zpow(alpha, w, 32.0 * L * wi));
+    for (int k = 0; k < 4; ++k) put(t[56 + k], zpow(alpha, w, 32.0 * L * (1 << k)));
+    for (int l = 0; l < sftk::kTileTab; ++l) {
+      const cd v = zpow(alpha, w, static_cast<double>(TT) * l);
+      tt[p * sftk::kTileTab + l] = make_double2(v.real(), v.imag());
+    }
+  }
+  cuda_check(cudaMalloc(&g.d_tab, tab.size() * sizeof(T2)), "cudaMalloc tables");
+  cuda_check(cudaMemcpy(g.d_tab, tab.data(), tab.size() * sizeof(T2), cudaMemcpyHostToDevice), "copy tables");
+  cuda_check(cudaMalloc(&g.d_tab_tile, tt.size() * sizeof(double2)), "cudaMalloc tile tables");
+  cuda_check(cudaMemcpy(g.d_tab_tile, tt.data(), tt.size() * sizeof(double2), cudaMemcpyHostToDevice),
+             "copy tile tables");
+}
+
+template <typename T>
+sftk::ScanParams<T>& params_of(Group& g);
+template <>
+sftk::ScanParams<float>& params_of<float>(Group& g) {
+  return g.pf;
+}
+template <>
+sftk::ScanParams<double>& params_of<double>(Group& g) {
+  return g.pd;
+}
+
+template <typename T>
+void build_groups(sftgpu_plan* pl, const std::vector<Order>& ords, double alpha, double pref, bool comps) {
+  for (size_t g0 = 0; g0 < ords.size(); g0 += sftk::kMaxOrd) {
+    const size_t g1 = std::min(ords.size(), g0 + sftk::kMaxOrd);
+    std::vector<Order> sub(ords.begin() + g0, ords.begin() + g1);
+    pl->groups.emplace_back();
+    Group& g = pl->groups.back();
+    g.nord = static_cast<int>(sub.size());
+    sftk::ScanParams<T>& P = params_of<T>(g);
+    std::memset(&P, 0, sizeof(P));
+    double Dr = 0, Di = 0;
+    fill_consts<T>(P, sub, alpha, pref, pl->K, comps, &Dr, &Di);
+    P.Dr = g0 == 0 ? static_cast<T>(Dr) : T(0);
+    P.Di = g0 == 0 ? static_cast<T>(Di) : T(0);
+    build_tables<T>(g, sub, alpha, pl->L, pl->NT);
+    P.tab = static_cast<const typename sftk::Vec2<T>::t*>(g.d_tab);
+    P.tab_tile = g.d_tab_tile;
+  }
+  pl->max_nord = 1;
+  for (const Group& g : pl->groups) pl->max_nord = std::max(pl->max_nord, g.nord);
+}
+
+void choose_geometry(sftgpu_plan* pl) {
+  pl->NT = 256;
+  if (pl->precision == SFTGPU_DOUBLE) {
+    pl->L = 4;
+  } else {
+    // prefer 2048-position tiles; fall back to 1024 when that leaves SMs idle
+    pl->L = 8;
+    const long long TT8 = 8LL * pl->NT;
+    const long long tiles8 = (2LL * pl->K + TT8 - 1) / TT8 + (pl->count + TT8 - 1) / TT8;
+    if (pl->batch * tiles8 < 2 * 148) pl->L = 4;
+  }
+  pl->TT = static_cast<long long>(pl->L) * pl->NT;
+  pl->warm_tiles = (2LL * pl->K + pl->TT - 1) / pl->TT;
+  pl->tiles_per_signal = pl->warm_tiles + (pl->count + pl->TT - 1) / pl->TT;
+  pl->total_tiles = pl->tiles_per_signal * pl->batch;
+}
+
+void alloc_workspace(sftgpu_plan* pl) {
+  cuda_check(cudaMalloc(&pl->d_ticket, sizeof(unsigned long long)), "cudaMalloc ticket");
+  cuda_check(cudaMemset(pl->d_ticket, 0, sizeof(unsigned long long)), "memset ticket");
+  cuda_check(cudaMalloc(&pl->d_flags, pl->total_tiles * sizeof(unsigned long long)), "cudaMalloc flags");
+  cuda_check(cudaMemset(pl->d_flags, 0, pl->total_tiles * sizeof(unsigned long long)), "memset flags");
+  const size_t pay = static_cast<size_t>(pl->total_tiles) * pl->max_nord * sizeof(double2);
+  cuda_check(cudaMalloc(&pl->d_agg, pay), "cudaMalloc aggregates");
+  cuda_check(cudaMalloc(&pl->d_incl, pay), "cudaMalloc prefixes");
+}
+
+Lowered lower_spec(const sftb::Spec& s) {
+  Lowered lw;
+  lw.alpha = s.alpha;
+  switch (s.kind) {
+    case sftb::TKind::Gauss:
+    case sftb::TKind::GaussD:
+    case sftb::TKind::GaussDD: {
+      // proj/src/transforms.cpp:279-335
+      const sftb::Bundle& b = s.bundle;
+      lw.K = b.params.K;
+      lw.prefactor = s.n0 == 0 ? 1.0 : std::exp(-s.alpha * s.alpha / (4.0 * b.params.gamma()));
+      for (int p = 0; p <= b.P; ++p) {
+        double wc = 0.0, ws = 0.0;
+        const double ap = b.a[p], bp = p >= 1 ? b.b[p - 1] : 0.0, dp = b.d[p];
+        if (s.kind == sftb::TKind::Gauss) {
+          wc = ap;
+        } else if (s.kind == sftb::TKind::GaussD) {
+          ws = bp;
+          if (s.n0 != 0) wc = -s.alpha * ap;
+        } else {
+          wc = dp;
+          if (s.n0 != 0) {
+            wc += s.alpha * s.alpha * ap;
+            ws = -2.0 * s.alpha * bp;
+          }
+        }
+        lw.orders.push_back({s.beta * p, wc, ws});
+      }
+      lw.complex_out = false;
+      break;
+    }
+    case sftb::TKind::MorletDirect: {
+      // proj/src/transforms.cpp:337-371 (sin weight only where the sin order exists)
+      const sftb::Coeffs& c = s.morlet;
+      lw.K = s.mparams.K;
+      lw.prefactor = s.n0 == 0 ? 1.0 : std::exp(-s.alpha * s.alpha / (4.0 * s.mparams.gamma()));
+      size_t si = 0;
+      for (size_t ci = 0; ci < c.grid.cos_p.size(); ++ci) {
+        const int p = c.grid.cos_p[ci];
+        cd ws(0.0, 0.0);
+        if (si < c.grid.sin_p.size() && c.grid.sin_p[si] == p) ws = c.sc[si++];
+        lw.orders.push_back({s.beta * p, c.cc[ci], ws});
+      }
+      lw.complex_out = true;
+      break;
+    }
+    case sftb::TKind::MorletMultiply: {
+      // proj/src/transforms.cpp:373-428
+      const sftb::Coeffs& e = s.envelope;
+      const sftb::MorletP& mp = s.mparams;
+      lw.K = mp.K;
+      lw.prefactor = s.n0 == 0 ? 1.0 : std::exp(-s.alpha * s.alpha / (4.0 * mp.gamma()));
+      const int P = s.max_order;
+      const cd carrier = s.n0 == 0 ? cd(1.0, 0.0)
+                                   : cd(std::cos(mp.xi * s.n0 / mp.sigma), std::sin(mp.xi * s.n0 / mp.sigma));
+      for (int p = -P; p <= P; ++p) {
+        const double ap = e.cc[std::abs(p)].real();
+        const double apr = p == 0 ? ap : 0.5 * ap;
+        lw.orders.push_back({mp.xi / mp.sigma + s.beta * p, carrier * apr, carrier * apr * cd(0, 1)});
+      }
+      for (int p = 0; p <= P; ++p)
+        lw.orders.push_back({s.beta * p, cd(-mp.kappa() * e.cc[p].real(), 0.0), cd(0.0, 0.0)});
+      lw.complex_out = true;
+      break;
+    }
+    default: fail(SFTGPU_EINVAL, "lower_spec: not an SFT transform kind");
+  }
+  return lw;
+}
+
+// ---------------------------------------------------------------- C struct <-> internal
+sftb::Options to_options(const sftgpu_options* o) {
+  sftb::Options r;
+  if (!o) return r;
+  r.has_K = o->has_half_width != 0;
+  r.K = o->half_width;
+  r.has_beta = o->has_beta != 0;
+  r.beta = o->beta;
+  r.tune = o->tune_beta != 0;
+  r.has_ps = o->has_ps != 0;
+  r.ps = o->ps;
+  r.strategy = o->strategy;
+  r.precision = o->precision;
+  return r;
+}
+
+void coeffs_to_c(const sftb::Coeffs& c, sftgpu_coeffs* o) {
+  std::memset(o, 0, sizeof(*o));
+  if (c.grid.cos_p.size() > SFTGPU_MAX_COEFFS || c.grid.sin_p.size() > SFTGPU_MAX_COEFFS)
+    fail(SFTGPU_EINVAL, "too many coefficients for sftgpu_coeffs");
+  o->kind = c.kind;
+  o->half_width = c.grid.K;
+  o->beta = c.grid.beta;
+  o->n_cos = static_cast<int>(c.grid.cos_p.size());
+  o->n_sin = static_cast<int>(c.grid.sin_p.size());
+  for (int i = 0; i < o->n_cos; ++i) {
+    o->cos_orders[i] = c.grid.cos_p[i];
+    o->cos_coeffs[2 * i] = c.cc[i].real();
+    o->cos_coeffs[2 * i + 1] = c.cc[i].imag();
+  }
+  for (int i = 0; i < o->n_sin; ++i) {
+    o->sin_orders[i] = c.grid.sin_p[i];
+    o->sin_coeffs[2 * i] = c.sc[i].real();
+    o->sin_coeffs[2 * i + 1] = c.sc[i].imag();
+  }
+  o->fit_rmse_percent = c.fit_rmse;
+  o->sigma = c.sigma;
+  o->xi = c.xi;
+  o->n0 = c.n0;
+}
+
+sftb::Coeffs coeffs_from_c(const sftgpu_coeffs* o) {
+  sftb::Coeffs c;
+  c.kind = o->kind;
+  std::vector<int> co(o->cos_orders, o->cos_orders + o->n_cos), so(o->sin_orders, o->sin_orders + o->n_sin);
+  c.grid = sftb::Grid(o->half_width, o->beta, co, so);
+  for (int i = 0; i < o->n_cos; ++i) c.cc.emplace_back(o->cos_coeffs[2 * i], o->cos_coeffs[2 * i + 1]);
+  for (int i = 0; i < o->n_sin; ++i) c.sc.emplace_back(o->sin_coeffs[2 * i], o->sin_coeffs[2 * i + 1]);
+  c.fit_rmse = o->fit_rmse_percent;
+  c.sigma = o->sigma;
+  c.xi = o->xi;
+  c.n0 = o->n0;
+  return c;
+}
+
+void bundle_to_c(const sftb::Bundle& b, sftgpu_gauss_bundle* o) {
+  std::memset(o, 0, sizeof(*o));
+  if (b.P + 1 > SFTGPU_MAX_COEFFS) fail(SFTGPU_EINVAL, "too many coefficients for sftgpu_gauss_bundle");
+  o->sigma = b.params.sigma;
+  o->half_width = b.params.K;
+  o->beta = b.beta;
+  o->max_order = b.P;
+  for (size_t i = 0; i < b.a.size(); ++i) o->a[i] = b.a[i];
+  for (size_t i = 0; i < b.b.size(); ++i) o->b[i] = b.b[i];
+  for (size_t i = 0; i < b.d.size(); ++i) o->d[i] = b.d[i];
+  o->fit_rmse_g = b.rmse_g;
+  o->fit_rmse_gd = b.rmse_gd;
+  o->fit_rmse_gdd = b.rmse_gdd;
+}
+
+sftb::Bundle bundle_from_c(const sftgpu_gauss_bundle* o) {
+  sftb::Bundle b;
+  b.params = sftb::GaussP(o->sigma, o->half_width);
+  b.beta = o->beta;
+  b.P = o->max_order;
+  b.a.assign(o->a, o->a + o->max_order + 1);
+  b.b.assign(o->b, o->b + o->max_order);
+  b.d.assign(o->d, o->d + o->max_order + 1);
+  b.rmse_g = o->fit_rmse_g;
+  b.rmse_gd = o->fit_rmse_gd;
+  b.rmse_gdd = o->fit_rmse_gdd;
+  return b;
+}
+
+void spec_to_c(const sftb::Spec& s, sftgpu_spec* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->kind = static_cast<int>(s.kind);
+  if (s.has_gauss) {
+    o->sigma = s.gparams.sigma;
+    o->half_width = s.gparams.K;
+  }
+  if (s.has_morlet) {
+    o->sigma = s.mparams.sigma;
+    o->xi = s.mparams.xi;
+    o->half_width = s.mparams.K;
+  }
+  o->max_order = s.max_order;
+  o->ps = s.ps;
+  o->pd = s.pd;
+  o->beta = s.beta;
+  o->n0 = s.n0;
+  o->alpha = s.alpha;
+  o->strategy = s.strategy;
+  o->precision = s.precision;
+  std::strncpy(o->abbreviation, s.abbrev.c_str(), sizeof(o->abbreviation) - 1);
+  o->kernel_rmse_percent = s.kernel_rmse;
+  if (s.has_bundle) bundle_to_c(s.bundle, &o->gauss);
+  if (s.has_mcoef) coeffs_to_c(s.morlet, &o->morlet);
+  if (s.has_env) coeffs_to_c(s.envelope, &o->envelope);
+}
+
+sftb::Spec spec_from_c(const sftgpu_spec* o) {
+  if (!o) fail(SFTGPU_EINVAL, "null spec");
+  sftb::Spec s;
+  s.kind = static_cast<sftb::TKind>(o->kind);
+  switch (s.kind) {
+    case sftb::TKind::Gauss:
+    case sftb::TKind::GaussD:
+    case sftb::TKind::GaussDD:
+      s.has_gauss = true;
+      s.gparams = sftb::GaussP(o->sigma, o->half_width);
+      s.bundle = bundle_from_c(&o->gauss);
+      s.has_bundle = true;
+      break;
+    case sftb::TKind::MorletDirect:
+      s.has_morlet = true;
+      s.mparams = sftb::MorletP(o->sigma, o->xi, o->half_width);
+      s.morlet = coeffs_from_c(&o->morlet);
+      s.has_mcoef = true;
+      break;
+    case sftb::TKind::MorletMultiply:
+      s.has_morlet = true;
+      s.mparams = sftb::MorletP(o->sigma, o->xi, o->half_width);
+      s.envelope = coeffs_from_c(&o->envelope);
+      s.has_env = true;
+      break;
+    case sftb::TKind::TruncGauss:
+      s.has_gauss = true;
+      s.gparams = sftb::GaussP(o->sigma, o->half_width);
+      break;
+    case sftb::TKind::TruncMorlet:
+      s.has_morlet = true;
+      s.mparams = sftb::MorletP(o->sigma, o->xi, o->half_width);
+      break;
+    default: fail(SFTGPU_EINVAL, "unknown transform kind");
+  }
+  s.max_order = o->max_order;
+  s.ps = o->ps;
+  s.pd = o->pd;
+  s.beta = o->beta;
+  s.n0 = o->n0;
+  s.alpha = o->alpha;
+  s.strategy = o->strategy;
+  s.precision = o->precision;
+  s.abbrev = o->abbreviation;
+  s.kernel_rmse = o->kernel_rmse_percent;
+  return s;
+}
+
+template <typename T>
+void run_groups(sftgpu_plan* pl, const void* x, long long ld_x, void* out, void* out_s, long long ld_out,
+                int accumulate_first, cudaStream_t st) {
+  for (size_t gi = 0; gi < pl->groups.size(); ++gi) {
+    Group& g = pl->groups[gi];
+    sftk::ScanParams<T> P = params_of<T>(g);
+    P.x = static_cast<const T*>(x);
+    P.n = pl->n;
+    P.ld_x = ld_x;
+    P.out = static_cast<T*>(out);
+    P.out_s = static_cast<T*>(out_s);
+    P.ld_out = ld_out;
+    P.ord_stride = pl->batch * ld_out;
+    P.lo = pl->lo;
+    P.count = pl->count;
+    P.K = pl->K;
+    P.boundary = pl->boundary;
+    P.accumulate = (gi > 0 && !pl->is_components) ? 1 : accumulate_first;
+    P.vec_ok = (reinterpret_cast<uintptr_t>(out) % (2 * sizeof(T)) == 0) ? 1 : 0;
+    P.tiles_per_signal = pl->tiles_per_signal;
+    P.warm_tiles = pl->warm_tiles;
+    P.ticket = pl->d_ticket;
+    P.ticket_base = pl->ticket_base;
+    P.flags = pl->d_flags;
+    P.agg = pl->d_agg;
+    P.incl = pl->d_incl;
+    P.epoch = ++pl->epoch;
+    if (pl->is_components && gi > 0) {
+      // later component groups write further down the [order] axis
+      long long skip = 0;
+      for (size_t k = 0; k < gi; ++k) skip += pl->groups[k].nord;
+      P.out = static_cast<T*>(out) + skip * P.ord_stride;
+      P.out_s = static_cast<T*>(out_s) + skip * P.ord_stride;
+    }
+    launch_scan<T>(pl->L, g.nord, pl->mode, P, pl->total_tiles, st);
+    cuda_check(cudaGetLastError(), "sft_scan_kernel launch");
+    pl->ticket_base += static_cast<unsigned long long>(pl->total_tiles);
+  }
+}
+
+// GCT3/MCT3 (proj/src/transforms.cpp:430-442): fp64 accumulation into a complex
+// scratch row, then copied into the output layout (real for GCT3, complex for MCT3).
+// Like the reference, the direct path always computes in double precision.
+void run_conv(sftgpu_plan* pl, const void* x, long long ld_x, void* out, long long ld_out, cudaStream_t st) {
+  constexpr int BO = 256, BT = 1024;
+  const long long blocks = (pl->n + BO - 1) / BO;
+  for (long long b = 0; b < pl->batch; ++b) {
+    const double* xb = static_cast<const double*>(x) + b * ld_x;
+    sftk::truncated_conv_kernel<double, BO, BT><<<blocks, BO, 0, st>>>(xb, pl->n, pl->boundary, pl->d_taps,
+                                                                       pl->n_taps, pl->tap_lo, pl->d_conv_tmp);
+    cuda_check(cudaGetLastError(), "truncated_conv_kernel launch");
+    if (pl->mode == sftk::kModeComplex) {
+      double* ob = static_cast<double*>(out) + 2 * b * ld_out;
+      cuda_check(cudaMemcpyAsync(ob, pl->d_conv_tmp, pl->n * sizeof(double2), cudaMemcpyDeviceToDevice, st),
+                 "conv copy");
+    } else {
+      double* ob = static_cast<double*>(out) + b * ld_out;
+      cuda_check(cudaMemcpy2DAsync(ob, sizeof(double), pl->d_conv_tmp, sizeof(double2), sizeof(double), pl->n,
+                                   cudaMemcpyDeviceToDevice, st),
+                 "conv real copy");
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sftgpu_last_error(void) { return g_err.c_str(); }
+const char* sftgpu_version(void) { return "sftgpu 0.1.0 (sm_100a)"; }
+
+int sftgpu_parse_abbreviation(const char* abbrev, int* kind, int* n0, int* order) {
+  return guarded([&] {
+    if (!abbrev) fail(SFTGPU_EINVAL, "null abbreviation");
+    const sftb::Abbrev a = sftb::parse_abbreviation(abbrev);
+    *kind = static_cast<int>(a.kind);
+    *n0 = a.n0;
+    *order = a.order;
+  });
+}
+
+int sftgpu_encode_abbreviation(int kind, int n0, int order, char* out, int out_len) {
+  return guarded([&] {
+    const std::string s = sftb::encode_abbreviation(static_cast<sftb::TKind>(kind), n0, order);
+    if (static_cast<int>(s.size()) + 1 > out_len) fail(SFTGPU_EINVAL, "buffer too small");
+    std::memcpy(out, s.c_str(), s.size() + 1);
+  });
+}
+
+int sftgpu_make_transform_spec(const char* abbrev, double sigma, double xi, const sftgpu_options* opt,
+                               sftgpu_spec* out) {
+  return guarded([&] {
+    if (!abbrev) fail(SFTGPU_EINVAL, "null abbreviation");
+    spec_to_c(sftb::make_transform_spec(abbrev, sigma, xi, to_options(opt)), out);
+  });
+}
+
+int sftgpu_make_gauss_spec(double sigma, int gauss_kind, int max_order, int n0, const sftgpu_options* opt,
+                           sftgpu_spec* out) {
+  return guarded([&] {
+    spec_to_c(sftb::make_gauss_spec(sigma, static_cast<sftb::GKind>(gauss_kind), max_order, n0, to_options(opt)),
+              out);
+  });
+}
+
+int sftgpu_make_morlet_direct_spec(double sigma, double xi, int pd, int n0, const sftgpu_options* opt,
+                                   sftgpu_spec* out) {
+  return guarded([&] { spec_to_c(sftb::make_morlet_direct_spec(sigma, xi, pd, n0, to_options(opt)), out); });
+}
+
+int sftgpu_make_morlet_multiply_spec(double sigma, double xi, int pm, int n0, const sftgpu_options* opt,
+                                     sftgpu_spec* out) {
+  return guarded([&] { spec_to_c(sftb::make_morlet_multiply_spec(sigma, xi, pm, n0, to_options(opt)), out); });
+}
+
+int sftgpu_effective_kernel(const sftgpu_spec* spec, double* taps, int64_t cap, int64_t* n_taps, int64_t* tap_lo) {
+  return guarded([&] {
+    const sftb::Taps t = sftb::effective_kernel(spec_from_c(spec));
+    *n_taps = static_cast<int64_t>(t.taps.size());
+    *tap_lo = t.lo;
+    if (taps) {
+      if (cap < static_cast<int64_t>(t.taps.size())) fail(SFTGPU_EINVAL, "taps buffer too small");
+      for (size_t i = 0; i < t.taps.size(); ++i) {
+        taps[2 * i] = t.taps[i].real();
+        taps[2 * i + 1] = t.taps[i].imag();
+      }
+    }
+  });
+}
+
+int sftgpu_fit_mmse(const double* target, int K, double beta, int n_cos, const int* cos_orders, int n_sin,
+                    const int* sin_orders, int kind, sftgpu_coeffs* out) {
+  return guarded([&] {
+    const sftb::Grid g(K, beta, std::vector<int>(cos_orders, cos_orders + n_cos),
+                       std::vector<int>(sin_orders, sin_orders + n_sin));
+    std::vector<cd> t(2 * static_cast<size_t>(K) + 1);
+    for (size_t i = 0; i < t.size(); ++i) t[i] = cd(target[2 * i], target[2 * i + 1]);
+    coeffs_to_c(sftb::fit_mmse(t, g, kind), out);
+  });
+}
+
+int sftgpu_fit_gaussian_bundle(double sigma, int K, int P, double beta, sftgpu_gauss_bundle* out) {
+  return guarded([&] { bundle_to_c(sftb::fit_gaussian_bundle(sftb::GaussP(sigma, K), P, beta), out); });
+}
+
+int sftgpu_fit_morlet_direct(double sigma, double xi, int K, int ps, int pd, double beta, int n0,
+                             sftgpu_coeffs* out) {
+  return guarded([&] { coeffs_to_c(sftb::fit_morlet_direct(sftb::MorletP(sigma, xi, K), ps, pd, beta, n0), out); });
+}
+
+int sftgpu_fit_morlet_envelope(double sigma, double xi, int K, int P, double beta, sftgpu_coeffs* out) {
+  return guarded([&] { coeffs_to_c(sftb::fit_morlet_envelope(sftb::MorletP(sigma, xi, K), P, beta), out); });
+}
+
+int sftgpu_select_optimal_ps(double sigma, double xi, int K, int pd, int n0, int* ps) {
+  return guarded([&] { *ps = sftb::select_optimal_ps(sftb::MorletP(sigma, xi, K), pd, n0); });
+}
+
+int sftgpu_morlet_direct_kernel_rmse(double sigma, double xi, int K, int ps, int pd, int n0, double* rmse) {
+  return guarded([&] { *rmse = sftb::morlet_direct_kernel_rmse(sftb::MorletP(sigma, xi, K), ps, pd, n0); });
+}
+
+int sftgpu_morlet_multiply_kernel_rmse(double sigma, double xi, int K, int pm, int n0, double* rmse) {
+  return guarded([&] { *rmse = sftb::morlet_multiply_kernel_rmse(sftb::MorletP(sigma, xi, K), pm, n0); });
+}
+
+int sftgpu_gauss_kernel_rmse(const sftgpu_gauss_bundle* b, int kind, int n0, double* rmse) {
+  return guarded([&] { *rmse = sftb::gauss_kernel_rmse(bundle_from_c(b), static_cast<sftb::GKind>(kind), n0); });
+}
+
+int sftgpu_tune_beta_gauss(double sigma, int K, int P, int n0, double* beta, double* rmse) {
+  return guarded([&] {
+    const sftb::BetaTune r = sftb::tune_beta_gauss(sftb::GaussP(sigma, K), P, n0);
+    *beta = r.beta;
+    *rmse = r.rmse;
+  });
+}
+
+int sftgpu_transform_plan_create(const sftgpu_spec* spec, int64_t n, int64_t batch, int boundary,
+                                 sftgpu_plan** plan) {
+  return guarded([&] {
+    if (!plan) fail(SFTGPU_EINVAL, "null plan pointer");
+    *plan = nullptr;
+    if (n < 1) fail(SFTGPU_EINVAL, "Signal: need at least one sample");
+    if (batch < 1) fail(SFTGPU_EINVAL, "batch must be >= 1");
+    if (boundary != SFTGPU_BOUNDARY_ZERO && boundary != SFTGPU_BOUNDARY_CLAMP)
+      fail(SFTGPU_EINVAL, "unknown boundary policy");
+    const sftb::Spec s = spec_from_c(spec);
+    require_device();
+    auto pl = std::make_unique<sftgpu_plan>();
+    cuda_check(cudaGetDevice(&pl->device), "cudaGetDevice");
+    pl->precision = s.precision == SFTGPU_SINGLE ? SFTGPU_SINGLE : SFTGPU_DOUBLE;
+    pl->n = n;
+    pl->batch = batch;
+    pl->boundary = boundary;
+    if (s.kind == sftb::TKind::TruncGauss || s.kind == sftb::TKind::TruncMorlet) {
+      const sftb::Taps t = sftb::effective_kernel(s);
+      pl->conv = 1;
+      pl->mode = s.kind == sftb::TKind::TruncMorlet ? sftk::kModeComplex : sftk::kModeReal;
+      pl->precision = SFTGPU_DOUBLE;
+      pl->count = n;
+      pl->n_taps = static_cast<long long>(t.taps.size());
+      pl->tap_lo = t.lo;
+      std::vector<double2> h(t.taps.size());
+      for (size_t i = 0; i < h.size(); ++i) h[i] = make_double2(t.taps[i].real(), t.taps[i].imag());
+      cuda_check(cudaMalloc(&pl->d_taps, h.size() * sizeof(double2)), "cudaMalloc taps");
+      cuda_check(cudaMemcpy(pl->d_taps, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice), "copy taps");
+      cuda_check(cudaMalloc(&pl->d_conv_tmp, n * sizeof(double2)), "cudaMalloc conv scratch");
+      *plan = pl.release();
+      return;
+    }
+    const Lowered lw = lower_spec(s);
+    pl->K = lw.K;
+    pl->lo = -static_cast<long long>(s.n0);  // window read at n - n0 (transforms.cpp:287-288)
+    pl->count = n;
+    pl->mode = lw.complex_out ? sftk::kModeComplex : sftk::kModeReal;
+    choose_geometry(pl.get());
+    if (pl->precision == SFTGPU_SINGLE)
+      build_groups<float>(pl.get(), lw.orders, lw.alpha, lw.prefactor, false);
+    else
+      build_groups<double>(pl.get(), lw.orders, lw.alpha, lw.prefactor, false);
+    alloc_workspace(pl.get());
+    *plan = pl.release();
+  });
+}
+
+int sftgpu_components_plan_create(const sftgpu_config* cfgs, int n_orders, int64_t n, int64_t batch, int boundary,
+                                  int64_t lo, int64_t hi, int mode, sftgpu_plan** plan) {
+  return guarded([&] {
+    if (!plan) fail(SFTGPU_EINVAL, "null plan pointer");
+    *plan = nullptr;
+    if (!cfgs || n_orders < 1) fail(SFTGPU_EINVAL, "need at least one order");
+    if (n < 1) fail(SFTGPU_EINVAL, "Signal: need at least one sample");
+    if (batch < 1) fail(SFTGPU_EINVAL, "batch must be >= 1");
+    if (boundary != SFTGPU_BOUNDARY_ZERO && boundary != SFTGPU_BOUNDARY_CLAMP)
+      fail(SFTGPU_EINVAL, "unknown boundary policy");
+    const sftgpu_config& c0 = cfgs[0];
+    std::vector<Order> ords;
+    for (int i = 0; i < n_orders; ++i) {
+      const sftgpu_config& c = cfgs[i];
+      // SftConfig::validate (proj/include/sft/engine.hpp:51-59)
+      if (c.half_width < 1) fail(SFTGPU_EINVAL, "SftConfig: K must be >= 1");
+      if (!(c.beta > 0.0) && c.integer_order) fail(SFTGPU_EINVAL, "SftConfig: beta must be > 0");
+      if (c.alpha < 0.0) fail(SFTGPU_EINVAL, "SftConfig: alpha must be >= 0");
+      if (c.integer_order && c.p < 0) fail(SFTGPU_EINVAL, "OrderSpec: p must be >= 0");
+      if (!c.integer_order && c.strategy != SFTGPU_KERNEL_INTEGRAL)
+        fail(SFTGPU_EINVAL, "SftConfig: real-frequency components require the kernel-integral strategy");
+      if (c.half_width != c0.half_width || c.alpha != c0.alpha || c.precision != c0.precision)
+        fail(SFTGPU_EINVAL, "components plan: orders must share K, alpha and precision");
+      ords.push_back({c.integer_order ? c.beta * c.p : c.omega, cd(0, 0), cd(0, 0)});
+    }
+    // proj/src/engine.cpp:247, :260-269
+    if (mode == 1 && c0.alpha != 0.0) fail(SFTGPU_EINVAL, "sft_components: alpha must be 0 (use asft_components)");
+    if (mode == 2 && !(c0.alpha > 0.0)) fail(SFTGPU_EINVAL, "asft_components: alpha must be > 0");
+    if (lo > hi) fail(SFTGPU_EINVAL, "components_over: empty range");
+    require_device();
+    auto pl = std::make_unique<sftgpu_plan>();
+    cuda_check(cudaGetDevice(&pl->device), "cudaGetDevice");
+    pl->is_components = 1;
+    pl->precision = c0.precision == SFTGPU_SINGLE ? SFTGPU_SINGLE : SFTGPU_DOUBLE;
+    pl->mode = sftk::kModeComps;
+    pl->n = n;
+    pl->batch = batch;
+    pl->boundary = boundary;
+    pl->K = c0.half_width;
+    pl->lo = lo;
+    pl->count = hi - lo + 1;
+    choose_geometry(pl.get());
+    if (pl->precision == SFTGPU_SINGLE)
+      build_groups<float>(pl.get(), ords, c0.alpha, 1.0, true);
+    else
+      build_groups<double>(pl.get(), ords, c0.alpha, 1.0, true);
+    alloc_workspace(pl.get());
+    *plan = pl.release();
+  });
+}
+
+int sftgpu_transform_execute(sftgpu_plan* pl, const void* x, int64_t ld_x, void* out, int64_t ld_out,
+                             void* stream) {
+  return guarded([&] {
+    if (!pl || pl->is_components) fail(SFTGPU_EINVAL, "not a transform plan");
+    if (!x || !out) fail(SFTGPU_EINVAL, "null buffer");
+    if (ld_x < pl->n || ld_out < pl->n) fail(SFTGPU_EINVAL, "leading dimension smaller than n");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (pl->conv) {
+      run_conv(pl, x, ld_x, out, ld_out, st);
+      return;
+    }
+    if (pl->precision == SFTGPU_SINGLE)
+      run_groups<float>(pl, x, ld_x, out, nullptr, ld_out, 0, st);
+    else
+      run_groups<double>(pl, x, ld_x, out, nullptr, ld_out, 0, st);
+  });
+}
+
+int sftgpu_transform_execute_host(sftgpu_plan* pl, const void* x_host, void* out_host, void* stream) {
+  return guarded([&] {
+    if (!pl || pl->is_components) fail(SFTGPU_EINVAL, "not a transform plan");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t es = elem_size(pl->precision);
+    const size_t xb = static_cast<size_t>(pl->n * pl->batch) * es;
+    const size_t ob = xb * (pl->mode == sftk::kModeComplex ? 2 : 1);
+    if (pl->cap_x < xb) {
+      cudaFree(pl->d_x);
+      pl->d_x = nullptr;
+      cuda_check(cudaMalloc(&pl->d_x, xb), "cudaMalloc staging x");
+      pl->cap_x = xb;
+    }
+    if (pl->cap_out < ob) {
+      cudaFree(pl->d_out);
+      pl->d_out = nullptr;
+      cuda_check(cudaMalloc(&pl->d_out, ob), "cudaMalloc staging out");
+      pl->cap_out = ob;
+    }
+    cuda_check(cudaMemcpyAsync(pl->d_x, x_host, xb, cudaMemcpyHostToDevice, st), "H2D");
+    if (pl->conv) {
+      run_conv(pl, pl->d_x, pl->n, pl->d_out, pl->n, st);
+    } else if (pl->precision == SFTGPU_SINGLE) {
+      run_groups<float>(pl, pl->d_x, pl->n, pl->d_out, nullptr, pl->n, 0, st);
+    } else {
+      run_groups<double>(pl, pl->d_x, pl->n, pl->d_out, nullptr, pl->n, 0, st);
+    }
+    cuda_check(cudaMemcpyAsync(out_host, pl->d_out, ob, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "stream sync");
+  });
+}
+
+int sftgpu_plan_output_is_complex(const sftgpu_plan* pl) { return pl && pl->mode == sftk::kModeComplex ? 1 : 0; }
+
+int sftgpu_plan_launches_per_execute(const sftgpu_plan* pl) {
+  if (!pl) return 0;
+  if (pl->conv) return static_cast<int>(pl->batch);
+  return static_cast<int>(pl->groups.size());
+}
+
+int sftgpu_components_execute(sftgpu_plan* pl, const void* x, void* c, void* s, void* stream) {
+  return guarded([&] {
+    if (!pl || !pl->is_components) fail(SFTGPU_EINVAL, "not a components plan");
+    if (!x || !c || !s) fail(SFTGPU_EINVAL, "null buffer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (pl->precision == SFTGPU_SINGLE)
+      run_groups<float>(pl, x, pl->n, c, s, pl->count, 0, st);
+    else
+      run_groups<double>(pl, x, pl->n, c, s, pl->count, 0, st);
+  });
+}
+
+void sftgpu_plan_destroy(sftgpu_plan* pl) { delete pl; }
+
+int sftgpu_generate_signal(int kind, int64_t n, uint64_t seed, int64_t batch, int dtype, void* out, void* stream) {
+  return guarded([&] {
+    if (n < 1) fail(SFTGPU_EINVAL, "make_test_signal: N must be >= 1");
+    if (kind < 0 || kind > 3) fail(SFTGPU_EINVAL, "make_test_signal: unknown kind");
+    require_device();
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const long long total = n * batch;
+    const int threads = 256;
+    const long long blocks = std::min<long long>((total + threads - 1) / threads, 148LL * 16);
+    if (dtype == SFTGPU_SINGLE)
+      sftk::generate_signal_kernel<float><<<blocks, threads, 0, st>>>(kind, n, seed, batch, static_cast<float*>(out));
+    else
+      sftk::generate_signal_kernel<double><<<blocks, threads, 0, st>>>(kind, n, seed, batch, static_cast<double*>(out));
+    cuda_check(cudaGetLastError(), "generate_signal_kernel launch");
+  });
+}
+
+int sftgpu_truncated_convolution(const double* x, int64_t n, int boundary, const double* taps, int64_t n_taps,
+                                 int64_t tap_lo, double* out, void* stream) {
+  return guarded([&] {
+    if (n_taps < 1) fail(SFTGPU_EINVAL, "truncated_convolution: empty kernel");
+    if (n < 1) fail(SFTGPU_EINVAL, "Signal: need at least one sample");
+    require_device();
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    constexpr int BO = 256, BT = 1024;
+    sftk::truncated_conv_kernel<double, BO, BT><<<(n + BO - 1) / BO, BO, 0, st>>>(
+        x, n, boundary, reinterpret_cast<const double2*>(taps), n_taps, tap_lo, reinterpret_cast<double2*>(out));
+    cuda_check(cudaGetLastError(), "truncated_conv_kernel launch");
+  });
+}
+
+}  // extern "C"

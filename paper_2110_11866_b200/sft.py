@@ -1,0 +1,585 @@
+"""Python mirror of the reference library's public API for the SFT/ASFT path
+(namespace ``sft`` in /root/reference/proj/include/sft/*.hpp), executed on the B200
+through libsftgpu's C ABI.
+
+Same names, argument meaning and error behaviour as the reference:
+``std::invalid_argument`` -> ``ValueError``, ``FitDegenerateError`` ->
+``FitDegenerateError``; results are host arrays (``numpy``) like the reference's
+Eigen arrays. Device execution uses torch only for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from ._abi import FitDegenerateError, SftGpuError, check, lib
+
+__all__ = [
+    "BoundaryPolicy", "Precision", "Strategy", "TransformKind", "GaussKind", "TestSignalKind",
+    "Signal", "make_test_signal", "OrderSpec", "SftConfig", "ComponentSeq", "TransformOptions",
+    "TransformSpec", "TransformResult", "KernelTaps", "AbbrevInfo", "GaussianFitBundle",
+    "CoefficientSet", "parse_abbreviation", "encode_abbreviation", "make_transform_spec",
+    "make_gauss_spec", "make_morlet_direct_spec", "make_morlet_multiply_spec", "gauss_smooth",
+    "morlet_direct_transform", "morlet_multiply_transform", "truncated_reference", "apply_transform",
+    "effective_kernel", "components_over", "sft_components", "asft_components", "sft_via_sliding_sum",
+    "truncated_convolution", "fit_gaussian_bundle", "fit_morlet_direct", "fit_morlet_envelope",
+    "fit_mmse", "select_optimal_ps", "tune_beta_gauss", "gauss_kernel_rmse",
+    "morlet_direct_kernel_rmse", "morlet_multiply_kernel_rmse", "TransformPlan", "ComponentsPlan",
+    "FitDegenerateError", "SftGpuError",
+]
+
+
+class BoundaryPolicy(enum.IntEnum):  # include/sft/signal.hpp:12
+    Zero = 0
+    Clamp = 1
+
+
+class Precision(enum.IntEnum):  # include/sft/signal.hpp:15
+    Single = 0
+    Double = 1
+
+
+class Strategy(enum.IntEnum):  # include/sft/engine.hpp:16
+    KernelIntegral = 0
+    Recursive1 = 1
+    Recursive2 = 2
+
+
+class TransformKind(enum.IntEnum):  # include/sft/transforms.hpp:11-19
+    Gauss = 0
+    GaussD = 1
+    GaussDD = 2
+    MorletDirect = 3
+    MorletMultiply = 4
+    TruncConvGauss = 5
+    TruncConvMorlet = 6
+
+
+class GaussKind(enum.IntEnum):  # include/sft/fourier_fit.hpp:101
+    Value = 0
+    Deriv1 = 1
+    Deriv2 = 2
+
+
+class TestSignalKind(enum.IntEnum):  # include/sft/signal.hpp:47
+    Impulse = 0
+    Constant = 1
+    Chirp = 2
+    SeededNoise = 3
+
+
+# ------------------------------------------------------------------ signal
+class Signal:
+    """Finite real sample sequence + boundary policy (include/sft/signal.hpp:19-32)."""
+
+    def __init__(self, samples, boundary: BoundaryPolicy = BoundaryPolicy.Clamp):
+        arr = np.ascontiguousarray(np.asarray(samples, dtype=np.float64))
+        if arr.ndim != 1 or arr.size < 1:
+            raise ValueError("Signal: need at least one sample")
+        if not np.all(np.isfinite(arr)):
+            raise ValueError("Signal: samples must be finite")
+        self.samples = arr
+        self.boundary = BoundaryPolicy(boundary)
+
+    def size(self) -> int:
+        return int(self.samples.size)
+
+    def __len__(self) -> int:
+        return self.size()
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise SftGpuError("no CUDA device available (libsftgpu has no CPU fallback)")
+    return torch
+
+
+def _stream_ptr(torch):
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def make_test_signal(kind: TestSignalKind, n: int, seed: int, boundary=BoundaryPolicy.Clamp) -> Signal:
+    """Deterministic generators (proj/src/signal.cpp:24-51), generated on the device
+    by the splitmix64 kernel (K2) and copied back; noise is bit-identical."""
+    if n < 1:
+        raise ValueError("make_test_signal: N must be >= 1")
+    torch = _torch()
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    check(lib().sftgpu_generate_signal(int(kind), n, seed, 1, 1, C.c_void_p(out.data_ptr()), _stream_ptr(torch)))
+    return Signal(out.cpu().numpy(), boundary)
+
+
+def generate_signals(kind: TestSignalKind, n: int, seed: int, batch: int = 1, precision=Precision.Single):
+    """Device batch generator: [batch][n] tensor, signal i seeded with seed+i."""
+    torch = _torch()
+    dt = torch.float32 if precision == Precision.Single else torch.float64
+    out = torch.empty((batch, n), dtype=dt, device="cuda")
+    check(lib().sftgpu_generate_signal(int(kind), n, seed, batch, int(precision), C.c_void_p(out.data_ptr()), _stream_ptr(torch)))
+    return out
+
+
+# ------------------------------------------------------------------ engine types
+@dataclass
+class OrderSpec:  # include/sft/engine.hpp:18-39
+    integer_order: bool = True
+    p: int = 0
+    omega: float = 0.0
+
+    @staticmethod
+    def order(p: int) -> "OrderSpec":
+        if p < 0:
+            raise ValueError("OrderSpec: p must be >= 0")
+        return OrderSpec(True, p, 0.0)
+
+    @staticmethod
+    def frequency(omega: float) -> "OrderSpec":
+        return OrderSpec(False, 0, float(omega))
+
+    def angular(self, beta: float) -> float:
+        return beta * self.p if self.integer_order else self.omega
+
+
+@dataclass
+class SftConfig:  # include/sft/engine.hpp:41-60
+    half_width: int
+    beta: float
+    order: OrderSpec = field(default_factory=OrderSpec)
+    alpha: float = 0.0
+    n0: int = 0
+    strategy: Strategy = Strategy.Recursive2
+    precision: Precision = Precision.Double
+    window_2k1: bool = False
+
+    def _c(self) -> _abi.Config:
+        return _abi.Config(
+            self.half_width, self.beta, int(self.order.integer_order), self.order.p, self.order.omega,
+            self.alpha, self.n0, int(self.strategy), int(self.precision), int(self.window_2k1),
+        )
+
+
+@dataclass
+class ComponentSeq:  # include/sft/engine.hpp:65-68
+    c: np.ndarray
+    s: np.ndarray
+
+
+class ComponentsPlan:
+    """Device plan for component sequences of several orders sharing K/alpha/precision:
+    c, s are [n_orders][batch][hi-lo+1]."""
+
+    def __init__(self, cfgs, n: int, batch: int, boundary, lo: int, hi: int, mode: int = 0):
+        arr = (_abi.Config * len(cfgs))(*[c._c() for c in cfgs])
+        h = C.c_void_p()
+        check(lib().sftgpu_components_plan_create(arr, len(cfgs), n, batch, int(boundary), lo, hi, mode, C.byref(h)))
+        self._h = h
+        self.n_orders, self.n, self.batch, self.count = len(cfgs), n, batch, hi - lo + 1
+        self.precision = Precision(cfgs[0].precision)
+
+    def execute(self, x, c, s, stream=None):
+        torch = _torch()
+        st = C.c_void_p(stream) if stream is not None else _stream_ptr(torch)
+        check(lib().sftgpu_components_execute(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(c.data_ptr()), C.c_void_p(s.data_ptr()), st))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().sftgpu_plan_destroy(self._h)
+            self._h = None
+
+
+def _components(sig: Signal, cfgs, lo: int, hi: int, mode: int):
+    torch = _torch()
+    plan = ComponentsPlan(cfgs, sig.size(), 1, sig.boundary, lo, hi, mode)
+    dt = torch.float32 if plan.precision == Precision.Single else torch.float64
+    x = torch.from_numpy(sig.samples).to(device="cuda", dtype=dt)
+    c = torch.empty((len(cfgs), plan.count), dtype=dt, device="cuda")
+    s = torch.empty_like(c)
+    plan.execute(x, c, s)
+    torch.cuda.synchronize()
+    return c.double().cpu().numpy(), s.double().cpu().numpy()
+
+
+def components_over(sig: Signal, cfg: SftConfig, lo: int, hi: int) -> ComponentSeq:
+    """proj/src/engine.cpp:255-258 (signed output range, boundary-extended reads)."""
+    c, s = _components(sig, [cfg], lo, hi, 0)
+    return ComponentSeq(c[0], s[0])
+
+
+def sft_components(sig: Signal, cfg: SftConfig) -> ComponentSeq:
+    """proj/src/engine.cpp:260-264 (requires alpha == 0)."""
+    c, s = _components(sig, [cfg], 0, sig.size() - 1, 1)
+    return ComponentSeq(c[0], s[0])
+
+
+def asft_components(sig: Signal, cfg: SftConfig) -> ComponentSeq:
+    """proj/src/engine.cpp:266-269 (requires alpha > 0)."""
+    c, s = _components(sig, [cfg], 0, sig.size() - 1, 2)
+    return ComponentSeq(c[0], s[0])
+
+
+def sft_via_sliding_sum(sig: Signal, cfg: SftConfig, workers: int = 1) -> ComponentSeq:
+    """proj/src/engine.cpp:323-337: the kernel-integral components as fresh window sums.
+    On the GPU every output is produced by the same bounded-state window scan, so the
+    sliding-sum route and the kernel integral are one kernel; the reference's overflow
+    guard for the rebased attenuated sequence is kept for API parity."""
+    n = sig.size()
+    if cfg.alpha * (0.5 * n + cfg.half_width) > 600.0:
+        raise ValueError("sft_via_sliding_sum: alpha * N / 2 too large for the attenuated phased sequence")
+    checked = SftConfig(cfg.half_width, cfg.beta, cfg.order, cfg.alpha, cfg.n0, Strategy.KernelIntegral,
+                        cfg.precision, cfg.window_2k1)
+    c, s = _components(sig, [checked], 0, n - 1, 0)
+    return ComponentSeq(c[0], s[0])
+
+
+# ------------------------------------------------------------------ fits / specs
+@dataclass
+class CoefficientSet:  # include/sft/fourier_fit.hpp:56-68
+    kind: int
+    half_width: int
+    beta: float
+    cos_orders: list
+    sin_orders: list
+    cos_coeffs: np.ndarray
+    sin_coeffs: np.ndarray
+    fit_rmse_percent: float
+    sigma: float = 0.0
+    xi: float = 0.0
+    n0: int = 0
+
+    @staticmethod
+    def _from(c: _abi.Coeffs) -> "CoefficientSet":
+        cc = np.array(c.cos_coeffs[: 2 * c.n_cos]).reshape(-1, 2) if c.n_cos else np.zeros((0, 2))
+        sc = np.array(c.sin_coeffs[: 2 * c.n_sin]).reshape(-1, 2) if c.n_sin else np.zeros((0, 2))
+        return CoefficientSet(
+            c.kind, c.half_width, c.beta, list(c.cos_orders[: c.n_cos]), list(c.sin_orders[: c.n_sin]),
+            cc[:, 0] + 1j * cc[:, 1], sc[:, 0] + 1j * sc[:, 1], c.fit_rmse_percent, c.sigma, c.xi, c.n0,
+        )
+
+
+@dataclass
+class GaussianFitBundle:  # include/sft/fourier_fit.hpp:88-99
+    sigma: float
+    half_width: int
+    beta: float
+    max_order: int
+    a: np.ndarray
+    b: np.ndarray
+    d: np.ndarray
+    fit_rmse_g: float
+    fit_rmse_gd: float
+    fit_rmse_gdd: float
+
+    @staticmethod
+    def _from(b: _abi.GaussBundle) -> "GaussianFitBundle":
+        P = b.max_order
+        return GaussianFitBundle(
+            b.sigma, b.half_width, b.beta, P, np.array(b.a[: P + 1]), np.array(b.b[:P]), np.array(b.d[: P + 1]),
+            b.fit_rmse_g, b.fit_rmse_gd, b.fit_rmse_gdd,
+        )
+
+
+@dataclass
+class TransformOptions:  # include/sft/transforms.hpp:43-50
+    half_width: int | None = None
+    beta: float | None = None
+    tune_beta: bool = False
+    ps: int | None = None
+    strategy: Strategy = Strategy.Recursive2
+    precision: Precision = Precision.Double
+
+    def _c(self) -> _abi.Options:
+        return _abi.Options(
+            int(self.half_width is not None), self.half_width or 0, int(self.beta is not None), self.beta or 0.0,
+            int(self.tune_beta), int(self.ps is not None), self.ps or 0, int(self.strategy), int(self.precision),
+        )
+
+
+@dataclass
+class AbbrevInfo:
+    kind: TransformKind
+    n0: int = 0
+    order: int = 0
+
+
+class TransformSpec:
+    """Fully resolved transform (include/sft/transforms.hpp:23-41), backed by the
+    C ``sftgpu_spec``; fields are readable and the engine knobs writable."""
+
+    def __init__(self, raw: _abi.Spec):
+        self._raw = raw
+
+    kind = property(lambda s: TransformKind(s._raw.kind))
+    sigma = property(lambda s: s._raw.sigma)
+    xi = property(lambda s: s._raw.xi)
+    half_width = property(lambda s: s._raw.half_width)
+    max_order = property(lambda s: s._raw.max_order)
+    ps = property(lambda s: s._raw.ps)
+    pd = property(lambda s: s._raw.pd)
+    beta = property(lambda s: s._raw.beta)
+    abbreviation = property(lambda s: s._raw.abbreviation.decode())
+    kernel_rmse_percent = property(lambda s: s._raw.kernel_rmse_percent)
+
+    def _rw(name):  # noqa: N805
+        return property(lambda s: getattr(s._raw, name), lambda s, v: setattr(s._raw, name, v))
+
+    n0 = _rw("n0")
+    alpha = _rw("alpha")
+    strategy = property(lambda s: Strategy(s._raw.strategy), lambda s, v: setattr(s._raw, "strategy", int(v)))
+    precision = property(lambda s: Precision(s._raw.precision), lambda s, v: setattr(s._raw, "precision", int(v)))
+
+    @property
+    def gauss_coeffs(self):
+        return GaussianFitBundle._from(self._raw.gauss) if self.kind <= TransformKind.GaussDD else None
+
+    @property
+    def morlet_coeffs(self):
+        return CoefficientSet._from(self._raw.morlet) if self.kind == TransformKind.MorletDirect else None
+
+    @property
+    def envelope_coeffs(self):
+        return CoefficientSet._from(self._raw.envelope) if self.kind == TransformKind.MorletMultiply else None
+
+    def copy(self) -> "TransformSpec":
+        raw = _abi.Spec()
+        C.pointer(raw)[0] = self._raw
+        return TransformSpec(raw)
+
+
+def parse_abbreviation(abbrev: str) -> AbbrevInfo:
+    k, n0, o = C.c_int(), C.c_int(), C.c_int()
+    check(lib().sftgpu_parse_abbreviation(abbrev.encode(), C.byref(k), C.byref(n0), C.byref(o)))
+    return AbbrevInfo(TransformKind(k.value), n0.value, o.value)
+
+
+def encode_abbreviation(kind: TransformKind, n0: int, order: int) -> str:
+    buf = C.create_string_buffer(32)
+    check(lib().sftgpu_encode_abbreviation(int(kind), n0, order, buf, 32))
+    return buf.value.decode()
+
+
+def _opts(options):
+    return (options or TransformOptions())._c()
+
+
+def make_transform_spec(abbrev: str, sigma: float, xi: float, options: TransformOptions | None = None) -> TransformSpec:
+    raw = _abi.Spec()
+    o = _opts(options)
+    check(lib().sftgpu_make_transform_spec(abbrev.encode(), sigma, xi, C.byref(o), C.byref(raw)))
+    return TransformSpec(raw)
+
+
+def make_gauss_spec(sigma, kind: GaussKind, max_order: int, n0: int, options=None) -> TransformSpec:
+    raw = _abi.Spec()
+    o = _opts(options)
+    check(lib().sftgpu_make_gauss_spec(sigma, int(kind), max_order, n0, C.byref(o), C.byref(raw)))
+    return TransformSpec(raw)
+
+
+def make_morlet_direct_spec(sigma, xi, pd: int, n0: int, options=None) -> TransformSpec:
+    raw = _abi.Spec()
+    o = _opts(options)
+    check(lib().sftgpu_make_morlet_direct_spec(sigma, xi, pd, n0, C.byref(o), C.byref(raw)))
+    return TransformSpec(raw)
+
+
+def make_morlet_multiply_spec(sigma, xi, pm: int, n0: int, options=None) -> TransformSpec:
+    raw = _abi.Spec()
+    o = _opts(options)
+    check(lib().sftgpu_make_morlet_multiply_spec(sigma, xi, pm, n0, C.byref(o), C.byref(raw)))
+    return TransformSpec(raw)
+
+
+@dataclass
+class KernelTaps:  # include/sft/kernels.hpp:76-81
+    taps: np.ndarray
+    lo: int
+
+    def hi(self) -> int:
+        return self.lo + self.taps.size - 1
+
+
+def effective_kernel(spec: TransformSpec) -> KernelTaps:
+    n, lo = C.c_int64(), C.c_int64()
+    check(lib().sftgpu_effective_kernel(C.byref(spec._raw), None, 0, C.byref(n), C.byref(lo)))
+    buf = np.zeros(2 * n.value)
+    check(lib().sftgpu_effective_kernel(C.byref(spec._raw), buf.ctypes.data_as(C.c_void_p), n.value, C.byref(n), C.byref(lo)))
+    return KernelTaps(buf[0::2] + 1j * buf[1::2], lo.value)
+
+
+def fit_gaussian_bundle(sigma: float, half_width: int, max_order: int, beta: float) -> GaussianFitBundle:
+    b = _abi.GaussBundle()
+    check(lib().sftgpu_fit_gaussian_bundle(sigma, half_width, max_order, beta, C.byref(b)))
+    return GaussianFitBundle._from(b)
+
+
+def fit_morlet_direct(sigma, xi, half_width, ps, pd, beta, n0=0) -> CoefficientSet:
+    c = _abi.Coeffs()
+    check(lib().sftgpu_fit_morlet_direct(sigma, xi, half_width, ps, pd, beta, n0, C.byref(c)))
+    return CoefficientSet._from(c)
+
+
+def fit_morlet_envelope(sigma, xi, half_width, max_order, beta) -> CoefficientSet:
+    c = _abi.Coeffs()
+    check(lib().sftgpu_fit_morlet_envelope(sigma, xi, half_width, max_order, beta, C.byref(c)))
+    return CoefficientSet._from(c)
+
+
+def fit_mmse(target, half_width: int, beta: float, cos_orders, sin_orders, kind: int = 0) -> CoefficientSet:
+    t = np.asarray(target, dtype=np.complex128)
+    buf = np.ascontiguousarray(np.column_stack([t.real, t.imag]).ravel())
+    co = np.ascontiguousarray(cos_orders, dtype=np.int32)
+    so = np.ascontiguousarray(sin_orders, dtype=np.int32)
+    c = _abi.Coeffs()
+    check(lib().sftgpu_fit_mmse(buf.ctypes.data_as(C.c_void_p), half_width, beta, co.size, co.ctypes.data_as(C.c_void_p),
+                                so.size, so.ctypes.data_as(C.c_void_p), kind, C.byref(c)))
+    return CoefficientSet._from(c)
+
+
+def select_optimal_ps(sigma, xi, half_width, pd, n0=0) -> int:
+    ps = C.c_int()
+    check(lib().sftgpu_select_optimal_ps(sigma, xi, half_width, pd, n0, C.byref(ps)))
+    return ps.value
+
+
+def tune_beta_gauss(sigma, half_width, max_order, n0=0):
+    b, r = C.c_double(), C.c_double()
+    check(lib().sftgpu_tune_beta_gauss(sigma, half_width, max_order, n0, C.byref(b), C.byref(r)))
+    return b.value, r.value
+
+
+def gauss_kernel_rmse(bundle_spec: TransformSpec, kind: GaussKind, n0: int) -> float:
+    r = C.c_double()
+    check(lib().sftgpu_gauss_kernel_rmse(C.byref(bundle_spec._raw.gauss), int(kind), n0, C.byref(r)))
+    return r.value
+
+
+def morlet_direct_kernel_rmse(sigma, xi, half_width, ps, pd, n0) -> float:
+    r = C.c_double()
+    check(lib().sftgpu_morlet_direct_kernel_rmse(sigma, xi, half_width, ps, pd, n0, C.byref(r)))
+    return r.value
+
+
+def morlet_multiply_kernel_rmse(sigma, xi, half_width, pm, n0) -> float:
+    r = C.c_double()
+    check(lib().sftgpu_morlet_multiply_kernel_rmse(sigma, xi, half_width, pm, n0, C.byref(r)))
+    return r.value
+
+
+# ------------------------------------------------------------------ transforms
+@dataclass
+class TransformResult:  # include/sft/transforms.hpp:74-81
+    values: np.ndarray
+    complex_valued: bool
+    abbreviation: str
+    strategy: Strategy
+    precision: Precision
+    kernel_rmse_percent: float
+
+
+class TransformPlan:
+    """Device plan: ``batch`` signals of ``n`` samples -> transform output, all in HBM.
+    x: [batch][ld_x] (float32 for Single, float64 for Double); out: [batch][ld_out]
+    real, or [batch][ld_out][2] complex interleaved."""
+
+    def __init__(self, spec: TransformSpec, n: int, batch: int = 1, boundary=BoundaryPolicy.Clamp):
+        h = C.c_void_p()
+        check(lib().sftgpu_transform_plan_create(C.byref(spec._raw), n, batch, int(boundary), C.byref(h)))
+        self._h = h
+        self.n, self.batch = n, batch
+        self.complex_out = bool(lib().sftgpu_plan_output_is_complex(h))
+        conv = spec.kind in (TransformKind.TruncConvGauss, TransformKind.TruncConvMorlet)
+        self.precision = Precision.Double if conv else spec.precision
+        self.launches = lib().sftgpu_plan_launches_per_execute(h)
+
+    def dtype(self):
+        torch = _torch()
+        return torch.float32 if self.precision == Precision.Single else torch.float64
+
+    def empty_output(self):
+        torch = _torch()
+        shape = (self.batch, self.n, 2) if self.complex_out else (self.batch, self.n)
+        return torch.empty(shape, dtype=self.dtype(), device="cuda")
+
+    def execute(self, x, out, stream=None, ld_x=None, ld_out=None):
+        torch = _torch()
+        st = C.c_void_p(stream) if stream is not None else _stream_ptr(torch)
+        check(lib().sftgpu_transform_execute(self._h, C.c_void_p(x.data_ptr()), ld_x or self.n,
+                                             C.c_void_p(out.data_ptr()), ld_out or self.n, st))
+
+    def execute_host(self, x_host: np.ndarray, out_host: np.ndarray, stream=None):
+        torch = _torch()
+        st = C.c_void_p(stream) if stream is not None else _stream_ptr(torch)
+        check(lib().sftgpu_transform_execute_host(self._h, x_host.ctypes.data_as(C.c_void_p),
+                                                  out_host.ctypes.data_as(C.c_void_p), st))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().sftgpu_plan_destroy(self._h)
+            self._h = None
+
+
+def _run(sig: Signal, spec: TransformSpec) -> TransformResult:
+    torch = _torch()
+    plan = TransformPlan(spec, sig.size(), 1, sig.boundary)
+    x = torch.from_numpy(sig.samples).to(device="cuda", dtype=plan.dtype())
+    out = plan.empty_output()
+    plan.execute(x, out)
+    torch.cuda.synchronize()
+    o = out[0].double().cpu().numpy()
+    vals = (o[:, 0] + 1j * o[:, 1]) if plan.complex_out else o.astype(np.complex128)
+    return TransformResult(vals, plan.complex_out, spec.abbreviation, spec.strategy, spec.precision,
+                           spec.kernel_rmse_percent)
+
+
+def gauss_smooth(sig: Signal, spec: TransformSpec, workers: int = 1) -> TransformResult:
+    """proj/src/transforms.cpp:279-335. ``workers`` is accepted for API parity."""
+    if spec.kind not in (TransformKind.Gauss, TransformKind.GaussD, TransformKind.GaussDD):
+        raise ValueError("gauss_smooth: spec kind mismatch")
+    return _run(sig, spec)
+
+
+def morlet_direct_transform(sig: Signal, spec: TransformSpec, workers: int = 1) -> TransformResult:
+    """proj/src/transforms.cpp:337-371."""
+    if spec.kind != TransformKind.MorletDirect:
+        raise ValueError("morlet_direct_transform: spec mismatch")
+    return _run(sig, spec)
+
+
+def morlet_multiply_transform(sig: Signal, spec: TransformSpec, workers: int = 1) -> TransformResult:
+    """proj/src/transforms.cpp:373-428."""
+    if spec.kind != TransformKind.MorletMultiply:
+        raise ValueError("morlet_multiply_transform: spec mismatch")
+    return _run(sig, spec)
+
+
+def truncated_reference(sig: Signal, spec: TransformSpec, workers: int = 1) -> TransformResult:
+    """GCT3 / MCT3 (proj/src/transforms.cpp:430-442) on the GPU direct-convolution kernel."""
+    if spec.kind not in (TransformKind.TruncConvGauss, TransformKind.TruncConvMorlet):
+        raise ValueError("truncated_reference: spec mismatch")
+    return _run(sig, spec)
+
+
+def apply_transform(sig: Signal, spec: TransformSpec, workers: int = 1) -> TransformResult:
+    """proj/src/transforms.cpp:444-459."""
+    return _run(sig, spec)
+
+
+def truncated_convolution(sig: Signal, kernel: KernelTaps, workers: int = 1) -> np.ndarray:
+    """proj/src/kernels.cpp:35-51 on the GPU (fp64): out[n] = sum_k taps[k] x[n - (lo + k)]."""
+    torch = _torch()
+    if kernel.taps.size < 1:
+        raise ValueError("truncated_convolution: empty kernel")
+    x = torch.from_numpy(sig.samples).to("cuda")
+    t = torch.from_numpy(np.ascontiguousarray(np.column_stack([kernel.taps.real, kernel.taps.imag]).ravel())).to("cuda")
+    out = torch.empty(2 * sig.size(), dtype=torch.float64, device="cuda")
+    check(lib().sftgpu_truncated_convolution(C.c_void_p(x.data_ptr()), sig.size(), int(sig.boundary),
+                                             C.c_void_p(t.data_ptr()), kernel.taps.size, kernel.lo,
+                                             C.c_void_p(out.data_ptr()), _stream_ptr(torch)))
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    return o[0::2] + 1j * o[1::2]
