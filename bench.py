@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 SFT/ASFT hot path (driver contract).
+
+Default workload = BASELINE.json's headline: the Morlet wavelet transform, method 1
+(direct, MDS5P6 ASFT, fp32), N=102400, sigma=8192, xi=10 — one step = one transform of
+one signal. ``--workload`` selects the other BASELINE configs (1, 2, 4, 5).
+
+Arms:
+  --impl ours (default)   the product: libsftgpu K1 kernel through the C ABI.
+  --impl reference        the reference's CPU path (restated in oracle/, the reference
+                          itself does not build here: no Eigen3) on all host threads.
+Multi-GPU: one process per GPU (torchrun); single-signal workloads run independent
+replicas ("replicas only"); the scalogram shards scales across ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_BYTES = 126 * 1024 * 1024
+PAPER_MS = 0.545  # PAPER.md:28-30, RTX 3090, N=102400, sigma=8192
+
+WORKLOADS = {
+    # BASELINE config 3 (headline)
+    "morlet_direct": dict(abbrev="MDS5P6", sigma=8192.0, xi=10.0, n=102400, batch=1, precision=0,
+                          desc="Morlet method 1 (direct, MDS5P6 ASFT, P_S auto=7, P_D=6) fp32, N=102400, sigma=8192, xi=10"),
+    # BASELINE config 1
+    "gauss_sft_fp64": dict(abbrev="GDP6", sigma=8192.0, xi=0.0, n=102400, batch=1, precision=1,
+                           desc="Gaussian smoothing SFT (GDP6) fp64, N=102400, sigma=8192"),
+    # BASELINE config 2 (the sigma=8192 member)
+    "gauss_asft_fp32": dict(abbrev="GDS10P6", sigma=8192.0, xi=0.0, n=102400, batch=1, precision=0,
+                            desc="Gaussian smoothing ASFT (GDS10P6) fp32, N=102400, sigma=8192"),
+    # BASELINE config 4
+    "morlet_multiply_batch": dict(abbrev="MMS5P3", sigma=8192.0, xi=10.0, n=102400, batch=4096, precision=0,
+                                  desc="Morlet method 2 (multiply, MMS5P3 ASFT) fp32, 4096 x N=102400, sigma=8192, xi=10"),
+}
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clocks and throttle reasons via NVML while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self.period = period_s
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nvml = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                self.reasons |= self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nvml:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nvml:
+            self.t.join()
+
+    def summary(self):
+        if not self.nvml:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload: str):
+    """Per-launch dram bytes of K1 from the committed ncu --set full capture (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        return d.get(workload, {}).get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+# ------------------------------------------------------------------ reference arm (CPU)
+def oracle_run(O, spec, x, workers):
+    """The reference's CPU transform (restated, oracle/) for one signal, with the
+    reference's default strategy (Recursive2, proj/src/eval.cpp:186-189)."""
+    k = int(spec.kind)
+    prec = int(spec.precision)
+    gamma = 1.0 / (2.0 * spec.sigma ** 2)
+    if k <= 2:
+        b = spec.gauss_coeffs
+        return O.gauss_smooth(x, 1, k, spec.half_width, spec.beta, spec.n0, spec.alpha, gamma, O.RECURSIVE2, prec,
+                              b.a, b.b, b.d, workers)
+    if k == 3:
+        c = spec.morlet_coeffs
+        return O.morlet_direct(x, 1, spec.half_width, spec.beta, spec.n0, spec.alpha, gamma, O.RECURSIVE2, prec,
+                               c.cos_orders, c.cos_coeffs, c.sin_orders, c.sin_coeffs, workers)
+    e = spec.envelope_coeffs
+    return O.morlet_multiply(x, 1, spec.half_width, spec.beta, spec.n0, spec.alpha, spec.sigma, spec.xi,
+                             O.RECURSIVE2, prec, e.cos_coeffs.real, workers)
+
+
+def cpu_measure(spec, w, steps, warmup, sample_signals):
+    """Times the CPU reference path on `sample_signals` signals per step, all host threads."""
+    import oracle as O
+
+    cores = os.cpu_count() or 1
+    xs = [O.make_test_signal(O.SEEDED_NOISE, w["n"], 1234 + i) for i in range(sample_signals)]
+    if w["precision"] == 0:
+        xs = [x.astype("float32").astype("float64") for x in xs]
+    for _ in range(warmup):
+        oracle_run(O, spec, xs[0], cores)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        for x in xs:
+            oracle_run(O, spec, x, cores)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return sample_signals * w["n"] / t / 1e6, t, cores
+
+
+def run_reference(args, w, spec_of):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return
+    spec = spec_of()
+    sample = 1 if w["batch"] == 1 else 2
+    value, t, cores = cpu_measure(spec, w, args.steps, args.warmup, sample)
+    line = {
+        "impl": "reference",
+        "metric": "Morlet transform ms @N=102400,σ=8192; Msamples·scales/s; HBM GB/s vs peak",
+        "value": value, "unit": "Msamples·scales/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3 / sample, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": value / (w["n"] / (PAPER_MS * 1e-3) / 1e6) if w["n"] == 102400 else None,
+        "dtype": "f32" if w["precision"] == 0 else "f64", "data": "synthetic (splitmix64 noise, seed 1234+i)",
+        "config": {"workload": args.workload, "desc": w["desc"], "strategy": "Recursive2 (reference default)"},
+        "cpu_baseline": {"value": value, "unit": "Msamples·scales/s", "cores": cores, "kind": "port",
+                         "sample": f"{sample} signal(s) of N={w['n']} per step, median of {args.steps}"},
+        "e2e": {"value": value, "unit": "Msamples·scales/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm (GPU)
+def run_ours(args, w, spec_of):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2110_11866_b200 as P
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    spec = spec_of()
+    n, batch = w["n"], w["batch"]
+    plan = P.TransformPlan(spec, n, batch)
+    in_es = 4 if w["precision"] == 0 else 8
+    out_es = in_es * (2 if plan.complex_out else 1)
+    step_bytes = batch * n * (in_es + out_es)
+    R = max(1, math.ceil(3 * L2_BYTES / step_bytes)) if step_bytes < 3 * L2_BYTES else 1
+    R = min(R, 512)
+    prec = P.Precision.Single if w["precision"] == 0 else P.Precision.Double
+    xs = [P.generate_signals(P.TestSignalKind.SeededNoise, n, 1234 + rank * 7919, batch, prec) for _ in range(min(R, 2))]
+    xs = [xs[i % len(xs)] if i < 2 else xs[i % 2].clone() for i in range(R)]
+    outs = [plan.empty_output() for _ in range(R)]
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            plan.execute(xs[i % R], outs[i % R])
+        stream.synchronize()
+        graph = None
+        if not args.no_graph:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                for k in range(args.steps):
+                    plan.execute(xs[k % R], outs[k % R])
+            graph.replay()  # one untimed replay (graph upload)
+            stream.synchronize()
+
+        def timed_region():
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            if graph is not None:
+                graph.replay()
+            else:
+                for k in range(args.steps):
+                    plan.execute(xs[k % R], outs[k % R])
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            return ev0.elapsed_time(ev1)
+
+        with ClockSampler(local) as clk:
+            ms = timed_region()
+            # keep the clock record meaningful for sub-second regions: sample a few more
+            # identical replays (not part of the reported number) only if too few samples
+            t_extra = time.perf_counter()
+            while len(clk.samples) < 20 and time.perf_counter() - t_extra < 2.0 and graph is not None:
+                graph.replay()
+                stream.synchronize()
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_per_step = ms / args.steps
+    samples = n * batch * args.steps * world
+    value = samples / (ms * 1e-3) / 1e6
+
+    # e2e through the C ABI with pinned host buffers (H2D + kernel + D2H + sync each step)
+    x_host = torch.empty((batch, n), dtype=plan.dtype()).pin_memory()
+    x_host.copy_(xs[0].cpu())
+    o_host = torch.empty(outs[0].shape, dtype=plan.dtype()).pin_memory()
+    e2e_steps = max(1, min(args.steps, 50 if step_bytes < 64 << 20 else 3))
+    with torch.cuda.stream(stream):
+        plan.execute_host(x_host.numpy(), o_host.numpy(), stream.cuda_stream)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            plan.execute_host(x_host.numpy(), o_host.numpy(), stream.cuda_stream)
+        e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = n * batch * e2e_steps * world / float(te.item()) / 1e6
+
+    peak, peak_src = measured_peaks()
+    launches = plan.launches
+    kernel_ms = ms_per_step / launches
+    achieved = step_bytes / launches / (kernel_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(args.workload)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        sample = 1 if batch == 1 else 2
+        cval, ct, cores = cpu_measure(spec, w, 3, 1, sample)
+        cpu = {"value": cval, "unit": "Msamples·scales/s", "cores": cores, "kind": "port",
+               "sample": f"{sample} signal(s) of N={n} per step (reference CPU path restated in oracle/, "
+                         f"Recursive2, all {cores} host threads), median of 3 after 1 warm-up",
+               "ms_per_signal": ct * 1e3 / sample}
+
+    if rank == 0:
+        line = {
+            "metric": "Morlet transform ms @N=102400,σ=8192; Msamples·scales/s; HBM GB/s vs peak",
+            "value": value, "unit": "Msamples·scales/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": (value / world) / (n / (PAPER_MS * 1e-3) / 1e6) if (n == 102400 and batch == 1) else None,
+            "dtype": "f32" if w["precision"] == 0 else "f64",
+            "data": "synthetic (device splitmix64 noise, bit-identical to make_test_signal)",
+            "config": {"workload": args.workload, "desc": w["desc"], "abbreviation": spec.abbreviation,
+                       "K": spec.half_width,
+                       "batch": batch, "n": n, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": (f"rotating {R} input/output buffer pairs ({R * step_bytes / 2**20:.0f} MiB > L2)"
+                              if R > 1 else "step working set larger than L2"),
+                       "timing": "CUDA graph of K steps, CUDA events on the launch stream, max over ranks"
+                       if graph is not None else "K launches, CUDA events, max over ranks"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": step_bytes / launches,
+                         "kernel": "sft_scan_kernel (K1)", "kernel_ms": kernel_ms},
+            "e2e": {"value": e2e_value, "unit": "Msamples·scales/s", "h2d_bytes_per_step": batch * n * in_es,
+                    "d2h_bytes_per_step": batch * n * out_es, "steps": e2e_steps,
+                    "path": "sftgpu_transform_execute_host (C ABI, pinned host buffers)"},
+            "gpu_launches": args.steps * launches,
+            "clocks": clk.summary(),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="morlet_direct")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    w = WORKLOADS[args.workload]
+
+    def spec_of():
+        import paper_2110_11866_b200 as P
+
+        return P.make_transform_spec(w["abbrev"], w["sigma"], w["xi"],
+                                     P.TransformOptions(precision=P.Precision(w["precision"]),
+                                                        strategy=P.Strategy.KernelIntegral))
+
+    if args.impl == "reference":
+        run_reference(args, w, spec_of)
+    else:
+        run_ours(args, w, spec_of)
+
+
+if __name__ == "__main__":
+    main()

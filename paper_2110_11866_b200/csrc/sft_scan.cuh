@@ -76,12 +76,14 @@ struct ScanParams {
   int vec_ok;  // output base/stride allow vector stores
   long long tiles_per_signal;
   long long warm_tiles;
-  unsigned long long* ticket;
-  unsigned long long ticket_base;
+  long long total_tiles;
+  // ctrl[0] tile ticket, ctrl[1] finished-CTA count, ctrl[2] launch epoch. The last
+  // CTA of a launch resets the ticket/count and bumps the epoch, so launches need no
+  // host-side state (graph-capturable) and stale look-back flags are ignored.
+  unsigned int* ctrl;
   unsigned long long* flags;
   double2* agg;
   double2* incl;
-  unsigned int epoch;
   const typename Vec2<T>::t* tab;
   const double2* tab_tile;
   T Dr, Di;
@@ -134,9 +136,9 @@ __device__ __forceinline__ double2 warp_sum2(double2 v) {
 // Per-order state lives in shared memory so the hot loops keep their registers.
 template <typename T, int NORD>
 __device__ __forceinline__ void lookback(const ScanParams<T>& P, long long gt, long long first,
-                                         const double2* s_agg, double2* s_run, double2* s_scl,
-                                         int lane) {
-  const unsigned long long ep = static_cast<unsigned long long>(P.epoch) << 32;
+                                         unsigned int epoch, const double2* s_agg, double2* s_run,
+                                         double2* s_scl, int lane) {
+  const unsigned long long ep = static_cast<unsigned long long>(epoch) << 32;
   if (gt == first) {
     if (lane < NORD) {
       P.incl[gt * NORD + lane] = s_agg[lane];
@@ -167,7 +169,7 @@ __device__ __forceinline__ void lookback(const ScanParams<T>& P, long long gt, l
     if (t >= first) {
       do {
         const unsigned long long f = ld_acquire_u64(P.flags + t);
-        st = (static_cast<unsigned int>(f >> 32) == P.epoch) ? static_cast<int>(f & 3ull) : 0;
+        st = (static_cast<unsigned int>(f >> 32) == epoch) ? static_cast<int>(f & 3ull) : 0;
       } while (st == 0);
     }
     __syncwarp();
@@ -219,14 +221,19 @@ __global__ void __launch_bounds__(NT) sft_scan_kernel(const __grid_constant__ Sc
   __shared__ T2 s_w[NW][NORD];
   __shared__ double2 s_lb[3][NORD];  // tile aggregate, carry, scale
   __shared__ long long s_tile;
+  __shared__ unsigned int s_epoch;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
 
-  if (tid == 0) s_tile = static_cast<long long>(atomicAdd(P.ticket, 1ull) - P.ticket_base);
+  if (tid == 0) {
+    s_tile = static_cast<long long>(atomicAdd(P.ctrl, 1u));
+    s_epoch = *reinterpret_cast<volatile unsigned int*>(P.ctrl + 2);
+  }
   __syncthreads();
   const long long gt = s_tile;
+  const unsigned int epoch = s_epoch;
   const long long sig = gt / P.tiles_per_signal;
   const long long first = sig * P.tiles_per_signal;
   const long long o0 = (gt - first - P.warm_tiles) * TT;  // first output index of this tile
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__(NT) sft_scan_kernel(const __grid_constant__ Sc
       if (lane == NW - 1) s_lb[0][p] = make_double2(static_cast<double>(v.x), static_cast<double>(v.y));
     }
     __syncwarp();
-    lookback<T, NORD>(P, gt, first, s_lb[0], s_lb[1], s_lb[2], lane);
+    lookback<T, NORD>(P, gt, first, epoch, s_lb[0], s_lb[1], s_lb[2], lane);
     if (lane < NW) {
 #pragma unroll 1
       for (int p = 0; p < NORD; ++p) {
@@ -339,6 +346,16 @@ __global__ void __launch_bounds__(NT) sft_scan_kernel(const __grid_constant__ Sc
     }
   }
   __syncthreads();
+  if (tid == 0) {
+    // every CTA has its ticket and has finished its look-back: the last one re-arms
+    __threadfence();
+    if (atomicAdd(P.ctrl + 1, 1u) == static_cast<unsigned int>(P.total_tiles - 1)) {
+      atomicExch(P.ctrl, 0u);
+      atomicExch(P.ctrl + 1, 0u);
+      atomicAdd(P.ctrl + 2, 1u);
+      __threadfence();
+    }
+  }
 
   if (o0 + TT <= 0) return;  // warm tile: no outputs
 

@@ -105,12 +105,10 @@ struct sftgpu_plan {
   long long TT = 1024, tiles_per_signal = 0, warm_tiles = 0, total_tiles = 0;
   std::vector<Group> groups;
   int max_nord = 1;
-  unsigned long long* d_ticket = nullptr;
+  unsigned int* d_ctrl = nullptr;  // ticket, done count, epoch (device-managed)
   unsigned long long* d_flags = nullptr;
   double2* d_agg = nullptr;
   double2* d_incl = nullptr;
-  unsigned long long ticket_base = 0;
-  unsigned int epoch = 0;
   // direct-convolution plans
   double2* d_taps = nullptr;
   long long n_taps = 0, tap_lo = 0;
@@ -126,7 +124,7 @@ struct sftgpu_plan {
       cudaFree(g.d_tab);
       cudaFree(g.d_tab_tile);
     }
-    cudaFree(d_ticket);
+    cudaFree(d_ctrl);
     cudaFree(d_flags);
     cudaFree(d_agg);
     cudaFree(d_incl);
@@ -275,8 +273,10 @@ void choose_geometry(sftgpu_plan* pl) {
 }
 
 void alloc_workspace(sftgpu_plan* pl) {
-  cuda_check(cudaMalloc(&pl->d_ticket, sizeof(unsigned long long)), "cudaMalloc ticket");
-  cuda_check(cudaMemset(pl->d_ticket, 0, sizeof(unsigned long long)), "memset ticket");
+  if (pl->total_tiles >= (1LL << 31)) fail(SFTGPU_EINVAL, "problem too large for one plan (tiles >= 2^31)");
+  const unsigned int ctrl0[4] = {0u, 0u, 1u, 0u};  // epoch starts at 1: zeroed flags are stale
+  cuda_check(cudaMalloc(&pl->d_ctrl, sizeof(ctrl0)), "cudaMalloc ctrl");
+  cuda_check(cudaMemcpy(pl->d_ctrl, ctrl0, sizeof(ctrl0), cudaMemcpyHostToDevice), "init ctrl");
   cuda_check(cudaMalloc(&pl->d_flags, pl->total_tiles * sizeof(unsigned long long)), "cudaMalloc flags");
   cuda_check(cudaMemset(pl->d_flags, 0, pl->total_tiles * sizeof(unsigned long long)), "memset flags");
   const size_t pay = static_cast<size_t>(pl->total_tiles) * pl->max_nord * sizeof(double2);
@@ -534,12 +534,11 @@ void run_groups(sftgpu_plan* pl, const void* x, long long ld_x, void* out, void*
     P.vec_ok = (reinterpret_cast<uintptr_t>(out) % (2 * sizeof(T)) == 0) ? 1 : 0;
     P.tiles_per_signal = pl->tiles_per_signal;
     P.warm_tiles = pl->warm_tiles;
-    P.ticket = pl->d_ticket;
-    P.ticket_base = pl->ticket_base;
+    P.total_tiles = pl->total_tiles;
+    P.ctrl = pl->d_ctrl;
     P.flags = pl->d_flags;
     P.agg = pl->d_agg;
     P.incl = pl->d_incl;
-    P.epoch = ++pl->epoch;
     if (pl->is_components && gi > 0) {
       // later component groups write further down the [order] axis
       long long skip = 0;
@@ -549,7 +548,6 @@ void run_groups(sftgpu_plan* pl, const void* x, long long ld_x, void* out, void*
     }
     launch_scan<T>(pl->L, g.nord, pl->mode, P, pl->total_tiles, st);
     cuda_check(cudaGetLastError(), "sft_scan_kernel launch");
-    pl->ticket_base += static_cast<unsigned long long>(pl->total_tiles);
   }
 }
 

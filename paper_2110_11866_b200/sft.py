@@ -20,7 +20,7 @@ from ._abi import FitDegenerateError, SftGpuError, check, lib
 
 __all__ = [
     "BoundaryPolicy", "Precision", "Strategy", "TransformKind", "GaussKind", "TestSignalKind",
-    "Signal", "make_test_signal", "OrderSpec", "SftConfig", "ComponentSeq", "TransformOptions",
+    "Signal", "make_test_signal", "generate_signals", "OrderSpec", "SftConfig", "ComponentSeq", "TransformOptions",
     "TransformSpec", "TransformResult", "KernelTaps", "AbbrevInfo", "GaussianFitBundle",
     "CoefficientSet", "parse_abbreviation", "encode_abbreviation", "make_transform_spec",
     "make_gauss_spec", "make_morlet_direct_spec", "make_morlet_multiply_spec", "gauss_smooth",
