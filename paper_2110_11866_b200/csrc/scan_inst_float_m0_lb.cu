@@ -1,0 +1,5 @@
+// Explicit instantiation of the K1 launcher: T=float, mode=0, SEQ=false (see scan_launch.cuh).
+#define SFTK_INSTANTIATE
+#include "scan_launch.cuh"
+template void sftk::launch_scan<float, 0, false>(const sftk::LaunchKey&, const sftk::ScanParams<float>&, long long,
+                                                  cudaStream_t);

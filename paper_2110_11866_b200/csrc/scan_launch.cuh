@@ -1,41 +1,65 @@
-// Launch dispatch for K1. Instantiated per (precision, mode) in scan_inst_*.cu so the
-// 72 kernel variants compile in parallel; sftgpu_api.cu only sees the declarations.
+// Launch dispatch for K1. Instantiated per (precision, mode, SEQ) in scan_inst_*.cu so
+// the kernel variants compile in parallel; sftgpu_api.cu only sees the declarations.
 #pragma once
 
 #include "sft_scan.cuh"
 
 namespace sftk {
 
-template <typename T, int MODE>
-void launch_scan(int L, int nord, const ScanParams<T>& p, long long grid, cudaStream_t s);
+// Tile geometry: NT threads x L positions. SEQ (batched) uses long tiles; LB (one
+// tile per CTA) uses shorter tiles so a single signal still spreads over the SMs.
+constexpr int kThreads = 128;
+constexpr int kLSeqF32 = 8, kLSeqF64 = 4;
+constexpr int kLLbF32 = 8, kLLbF64 = 4;
 
-#ifdef SFTK_INSTANTIATE
-template <typename T, int NORD, int MODE>
-static void launch_fixed(int L, const ScanParams<T>& p, long long grid, cudaStream_t s) {
-  if constexpr (sizeof(T) == 4) {
-    if (L == 8) {
-      sft_scan_kernel<T, NORD, MODE, 8, 256><<<grid, 256, 0, s>>>(p);
-      return;
-    }
-  }
-  sft_scan_kernel<T, NORD, MODE, 4, 256><<<grid, 256, 0, s>>>(p);
+template <typename T, bool SEQ>
+constexpr int lanes_per_thread() {
+  return sizeof(T) == 4 ? (SEQ ? kLSeqF32 : kLLbF32) : (SEQ ? kLSeqF64 : kLLbF64);
 }
 
-template <typename T, int MODE>
-void launch_scan(int L, int nord, const ScanParams<T>& p, long long grid, cudaStream_t s) {
-  switch (nord) {
-    case 1: launch_fixed<T, 1, MODE>(L, p, grid, s); break;
-    case 2: launch_fixed<T, 2, MODE>(L, p, grid, s); break;
-    case 3: launch_fixed<T, 3, MODE>(L, p, grid, s); break;
-    case 4: launch_fixed<T, 4, MODE>(L, p, grid, s); break;
-    case 5: launch_fixed<T, 5, MODE>(L, p, grid, s); break;
-    case 6: launch_fixed<T, 6, MODE>(L, p, grid, s); break;
-    case 7: launch_fixed<T, 7, MODE>(L, p, grid, s); break;
-    case 8: launch_fixed<T, 8, MODE>(L, p, grid, s); break;
-    case 9: launch_fixed<T, 9, MODE>(L, p, grid, s); break;
-    case 10: launch_fixed<T, 10, MODE>(L, p, grid, s); break;
-    case 11: launch_fixed<T, 11, MODE>(L, p, grid, s); break;
-    default: launch_fixed<T, 12, MODE>(L, p, grid, s); break;
+// Group mode 1 (split injection) is instantiated for the multiplication method's layout:
+// NORD = 3P+2 orders of which the first P+1 (kappa terms) use the real constant.
+constexpr int split_na(int nord) { return (nord % 3 == 2) ? (nord + 1) / 3 : -1; }
+
+struct LaunchKey {
+  int nord, gm, mode, seq;
+};
+
+template <typename T, int MODE, bool SEQ>
+void launch_scan(const LaunchKey& key, const ScanParams<T>& p, long long grid, cudaStream_t s);
+
+#ifdef SFTK_INSTANTIATE
+template <typename T, int NORD, int GM, int MODE, bool SEQ>
+static void launch_fixed(const ScanParams<T>& p, long long grid, cudaStream_t s) {
+  constexpr int L = lanes_per_thread<T, SEQ>();
+  constexpr int NA = GM == kGroupShared ? NORD : (GM == kGroupSplit ? split_na(NORD) : 0);
+  sft_scan_kernel<T, NORD, NA, GM, MODE, L, kThreads, SEQ><<<grid, kThreads, 0, s>>>(p);
+}
+
+template <typename T, int NORD, int MODE, bool SEQ>
+static void launch_gm(int gm, const ScanParams<T>& p, long long grid, cudaStream_t s) {
+  if constexpr (MODE == kModeComplex && split_na(NORD) > 0) {
+    if (gm == kGroupSplit) return launch_fixed<T, NORD, kGroupSplit, MODE, SEQ>(p, grid, s);
+  }
+  if (gm == kGroupShared) return launch_fixed<T, NORD, kGroupShared, MODE, SEQ>(p, grid, s);
+  launch_fixed<T, NORD, kGroupPerOrder, MODE, SEQ>(p, grid, s);
+}
+
+template <typename T, int MODE, bool SEQ>
+void launch_scan(const LaunchKey& key, const ScanParams<T>& p, long long grid, cudaStream_t s) {
+  switch (key.nord) {
+    case 1: launch_gm<T, 1, MODE, SEQ>(key.gm, p, grid, s); break;
+    case 2: launch_gm<T, 2, MODE, SEQ>(key.gm, p, grid, s); break;
+    case 3: launch_gm<T, 3, MODE, SEQ>(key.gm, p, grid, s); break;
+    case 4: launch_gm<T, 4, MODE, SEQ>(key.gm, p, grid, s); break;
+    case 5: launch_gm<T, 5, MODE, SEQ>(key.gm, p, grid, s); break;
+    case 6: launch_gm<T, 6, MODE, SEQ>(key.gm, p, grid, s); break;
+    case 7: launch_gm<T, 7, MODE, SEQ>(key.gm, p, grid, s); break;
+    case 8: launch_gm<T, 8, MODE, SEQ>(key.gm, p, grid, s); break;
+    case 9: launch_gm<T, 9, MODE, SEQ>(key.gm, p, grid, s); break;
+    case 10: launch_gm<T, 10, MODE, SEQ>(key.gm, p, grid, s); break;
+    case 11: launch_gm<T, 11, MODE, SEQ>(key.gm, p, grid, s); break;
+    default: launch_gm<T, 12, MODE, SEQ>(key.gm, p, grid, s); break;
   }
 }
 #endif

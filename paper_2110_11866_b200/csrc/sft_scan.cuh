@@ -9,16 +9,26 @@
 //
 // Math. Per order p with z = e^{-alpha - i omega}:
 //   y[n]  = sum_{k=-K..K} x[n-k] z^k            (c = Re y, s = -Im y, engine.hpp:62-68)
-//   V[n]  = sum_{j=n-K+1..n+K} x[j] z^{n+K-j}    (2K window, bounded state)
-//   V[n]  = z V[n-1] + x[n+K] - z^{2K} x[n-K]   (first-order linear recurrence)
+//   V[n]  = sum_{j=n-K+1..n+K} x[j] z^{n+K-j}    (2K window: state bounded by the window)
+//   V[n]  = z V[n-1] + g[n],  g[n] = x[n+K] - z^{2K} x[n-K]
 //   y[n]  = z^{-K} V[n] + z^{K} x[n-K]
-// The combine sum_p wc_p c_p + ws_p s_p is folded into 4 real weights per order
-// on (Re V, Im V) plus one complex weight D on x[n-K] shared by all orders.
-// The recurrence is evaluated as a parallel scan: per-thread Horner over L
-// positions, warp shuffle scan, inter-warp scan, and a decoupled look-back over
-// tiles (aggregates/inclusive prefixes in fp64) for the carry between CTAs.
+// For integer orders with beta = pi/K every order shares the real injection constant
+// z^{2K} = e^{-2 alpha K}, so g is computed once per position for all orders (group
+// mode 0); the multiplication method's real-frequency orders share one complex
+// constant (group mode 1); anything else uses per-order injection (group mode 2).
+// The combine sum_p wc_p c_p + ws_p s_p is folded into 4 real weights per order on
+// (Re V, Im V) plus one complex weight D on x[n-K] shared by all orders.
+//
+// Parallel structure: a tile of TT = NT*L positions per CTA step; per thread the
+// aggregate of its L positions is a dot product with precomputed z^{L-1-i} weights,
+// then a warp shuffle scan, an inter-warp scan, and the tile carry. Two modes:
+//   SEQ  one CTA owns a whole signal and walks its tiles with the carry in shared
+//        memory (fp64) and the next tile's samples prefetched in registers — batched
+//        workloads, no inter-CTA communication at all;
+//   LB   one tile per CTA and a decoupled look-back over tiles (fp64 aggregates /
+//        inclusive prefixes) — single long signals and small batches.
 // The signal is consumed from a virtual zero state 2K positions before the first
-// output ("warm tiles"), which makes the state at the first output exact.
+// output ("warm tiles", phase 1 only), which makes the state at the first output exact.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -28,10 +38,11 @@
 namespace sftk {
 
 constexpr int kMaxOrd = 12;
-constexpr int kTabStride = 64;  // table entries per order (see TableLayout)
-constexpr int kTileTab = 33;    // z^{T l}, l = 0..32
+constexpr int kMaxL = 8;
+constexpr int kTabStride = 64;  // table entries per order (see layout below)
 
 enum Mode { kModeReal = 0, kModeComplex = 1, kModeComps = 2 };
+enum GroupMode { kGroupShared = 0, kGroupSplit = 1, kGroupPerOrder = 2 };
 
 template <typename T>
 struct Vec2;
@@ -44,21 +55,31 @@ struct Vec2<double> {
   using t = double2;
 };
 
-// Hot per-order constants (kernel parameter space -> constant bank operands).
+// Hot per-order constants (kernel parameter space -> constant-bank operands).
 // Transform modes: k1..k4 map (Re V, Im V) to (Re out, Im out).
 // Components mode: k1 = Re a, k2 = Im a, k3 = Re b, k4 = Im b with a = z^{-K}, b = z^{K}.
+// Stored as the packed pairs the fp32 path feeds to FFMA2 (fma.rn.f32x2):
+//   zz = {zr, zr}, zx = {-zi, zi}, ka = {k1, k3}, kb = {k2, k4}, cc = {cr, ci},
+//   w[i] = {Re, Im, -Im, Re} of z^{L-1-i}.
 template <typename T>
 struct OrdConst {
-  T zr, zi;  // z
-  T cr, ci;  // z^{2K} (trailing-sample injection)
-  T k1, k2, k3, k4;
+  T zz[2];
+  T zx[2];
+  T ka[2];
+  T kb[2];
+  T cc[2];  // z^{2K} (per-order injection, group mode 2)
+  T w[kMaxL][4];
+  T scan[5][4];   // z^{L 2^k}, warp-scan multipliers, as {re, re, -im, im}
+  T wrot[4][4];   // z^{32 L w}, per-warp carry rotation (NW <= 4)
+  T m32[4];       // z^{32 L}, inter-warp step
 };
 
-// Table layout per order (T2 entries, stride kTabStride):
+// Table layout per order (entries {re, re, -im, im}, stride kTabStride):
 //   [ 0, 32)  z^{L*lane}
 //   [32, 37)  z^{L*2^k}      warp-scan multipliers
 //   [40, 56)  z^{32L*w}      per-warp carry rotation, w < NW
 //   [56, 60)  z^{32L*2^k}    inter-warp scan multipliers
+// Tile table (double2, per order): [0] z^{TT}, [1] z^{32 TT}.
 template <typename T>
 struct ScanParams {
   const T* x;
@@ -73,19 +94,21 @@ struct ScanParams {
   int K;
   int boundary;  // 0 zero, 1 clamp
   int accumulate;
-  int vec_ok;  // output base/stride allow vector stores
+  int vec_ok;  // output base and row stride allow 16-byte vector stores
+  int na;  // group mode 1: orders [0, na) use injection A, [na, NORD) injection B
   long long tiles_per_signal;
   long long warm_tiles;
-  long long total_tiles;
-  // ctrl[0] tile ticket, ctrl[1] finished-CTA count, ctrl[2] launch epoch. The last
-  // CTA of a launch resets the ticket/count and bumps the epoch, so launches need no
-  // host-side state (graph-capturable) and stale look-back flags are ignored.
+  long long total_tiles;  // LB: tiles in the grid
+  // ctrl[0] ticket, ctrl[1] finished-CTA count, ctrl[2] launch epoch. The last CTA
+  // of a launch resets ticket/count and bumps the epoch, so launches need no host
+  // state (graph-capturable) and stale look-back flags are ignored.
   unsigned int* ctrl;
   unsigned long long* flags;
   double2* agg;
   double2* incl;
-  const typename Vec2<T>::t* tab;
+  const T* tab;  // [NORD][kTabStride][4] entries {re, re, -im, im}
   const double2* tab_tile;
+  T cAr, cAi, cBr, cBi;  // shared injection constants (group modes 0/1)
   T Dr, Di;
   OrdConst<T> oc[kMaxOrd];
 };
@@ -100,9 +123,36 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Leading samples are re-read 2K positions later as trailing samples: keep them in L2
+// (evict_last policy); trailing reads are their last use and outputs are written once
+// (streaming), so neither displaces the signal window still needed.
+__device__ __forceinline__ unsigned long long l2_keep_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ float ld_keep(const float* p, unsigned long long pol) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_keep(const double* p, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 template <typename T>
 __device__ __forceinline__ T load_ext(const T* __restrict__ xs, long long n, int bnd, long long j) {
-  if (j >= 0 && j < n) return __ldg(xs + j);
+  if (j >= 0 && j < n) return __ldcs(xs + j);
+  if (bnd == 0) return T(0);
+  return __ldg(xs + (j < 0 ? 0 : n - 1));
+}
+
+template <typename T>
+__device__ __forceinline__ T load_ext_keep(const T* __restrict__ xs, long long n, int bnd, long long j,
+                                           unsigned long long pol) {
+  if (j >= 0 && j < n) return ld_keep(xs + j, pol);
   if (bnd == 0) return T(0);
   return __ldg(xs + (j < 0 ? 0 : n - 1));
 }
@@ -120,29 +170,64 @@ __device__ __forceinline__ T2 make2(decltype(T2::x) a, decltype(T2::x) b) {
   return r;
 }
 
-__device__ __forceinline__ double2 warp_sum2(double2 v) {
-#pragma unroll
-  for (int d = 16; d >= 1; d >>= 1) {
-    v.x += __shfl_xor_sync(0xffffffffu, v.x, d);
-    v.y += __shfl_xor_sync(0xffffffffu, v.y, d);
-  }
-  return v;
+// ---- packed fp32 pairs (FFMA2). ptxas folds the half swaps / broadcasts into operand
+// modifiers (.F32x2.LO_HI, .F32), so a complex multiply-add is two FFMA2.
+using u64 = unsigned long long;
+__device__ __forceinline__ u64 pk(float lo, float hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float plo(u64 v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return lo;
+}
+__device__ __forceinline__ float phi(u64 v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return hi;
+}
+__device__ __forceinline__ u64 pswap(u64 v) { return pk(phi(v), plo(v)); }
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ u64 ldp(const float* p) { return *reinterpret_cast<const u64*>(p); }
+// v + w * u for complex w = (wr, wi) given as packed {wr, wi}
+__device__ __forceinline__ u64 cmadd2(float wr, float wi, u64 u, u64 v) {
+  return fma2(pk(-wi, wi), pswap(u), fma2(pk(wr, wr), u, v));
 }
 
-// Decoupled look-back (one warp). Publishes this tile's aggregate s_agg, resolves
-// the exclusive carry (state at the end of the previous tile) from predecessors'
-// aggregates / inclusive prefixes into s_run, then publishes this tile's inclusive
-// prefix. Flags: (epoch << 32) | status, status 1 = aggregate, 2 = inclusive.
-// Per-order state lives in shared memory so the hot loops keep their registers.
-template <typename T, int NORD>
-__device__ __forceinline__ void lookback(const ScanParams<T>& P, long long gt, long long first,
-                                         unsigned int epoch, const double2* s_agg, double2* s_run,
-                                         double2* s_scl, int lane) {
-  const unsigned long long ep = static_cast<unsigned long long>(epoch) << 32;
+template <typename T, int NORD, int L, int NT>
+struct Smem {
+  using T2 = typename Vec2<T>::t;
+  static constexpr int TT = NT * L;
+  static constexpr int PAD = TT + TT / 32;
+  static constexpr int NW = NT / 32;
+  T lead[2][PAD];  // double-buffered sample staging (tile parity)
+  T trail[2][PAD];
+  T2 w[NW][NORD];         // warp totals, then per-warp carries
+  double2 carry[NORD];    // state at the end of the previous tile (fp64)
+  double2 tagg[NORD];     // this tile's aggregate
+  double2 pay[32][NORD];  // look-back payload staging
+  long long tile;
+  unsigned int epoch;
+};
+
+// Decoupled look-back over tiles (warp 0 of an LB-mode CTA). Publishes the tile
+// aggregate, resolves the carry (state at the end of the previous tile) from the
+// predecessors' aggregates / inclusive prefixes, publishes the inclusive prefix.
+// Flags: (epoch << 32) | status, status 1 = aggregate, 2 = inclusive.
+template <typename T, int NORD, int L, int NT>
+__device__ __forceinline__ void lookback(const ScanParams<T>& P, Smem<T, NORD, L, NT>& S, long long gt,
+                                         long long first, int lane) {
+  const unsigned long long ep = static_cast<unsigned long long>(S.epoch) << 32;
   if (gt == first) {
     if (lane < NORD) {
-      P.incl[gt * NORD + lane] = s_agg[lane];
-      s_run[lane] = make_double2(0.0, 0.0);
+      P.incl[gt * NORD + lane] = S.tagg[lane];
+      S.carry[lane] = make_double2(0.0, 0.0);
     }
     __syncwarp();
     if (lane == 0) {
@@ -152,16 +237,15 @@ __device__ __forceinline__ void lookback(const ScanParams<T>& P, long long gt, l
     __syncwarp();
     return;
   }
-  if (lane < NORD) {
-    P.agg[gt * NORD + lane] = s_agg[lane];
-    s_run[lane] = make_double2(0.0, 0.0);
-    s_scl[lane] = make_double2(1.0, 0.0);
-  }
+  if (lane < NORD) P.agg[gt * NORD + lane] = S.tagg[lane];
   __syncwarp();
   if (lane == 0) {
     __threadfence();
     st_release_u64(P.flags + gt, ep | 1ull);
   }
+  double2 run = make_double2(0.0, 0.0), scl = make_double2(1.0, 0.0);
+  const double2 zT = lane < NORD ? P.tab_tile[lane * 2] : make_double2(1.0, 0.0);
+  const double2 z32T = lane < NORD ? P.tab_tile[lane * 2 + 1] : make_double2(1.0, 0.0);
   long long base = gt - 1;
   while (true) {
     const long long t = base - lane;
@@ -169,35 +253,33 @@ __device__ __forceinline__ void lookback(const ScanParams<T>& P, long long gt, l
     if (t >= first) {
       do {
         const unsigned long long f = ld_acquire_u64(P.flags + t);
-        st = (static_cast<unsigned int>(f >> 32) == epoch) ? static_cast<int>(f & 3ull) : 0;
+        st = (static_cast<unsigned int>(f >> 32) == S.epoch) ? static_cast<int>(f & 3ull) : 0;
       } while (st == 0);
     }
-    __syncwarp();
     const unsigned inc = __ballot_sync(0xffffffffu, st >= 2);
     const int m = inc ? __ffs(inc) - 1 : 31;
-    const bool take = lane <= m && st != 3;
-    const double2* src = (st == 2) ? P.incl : P.agg;
-#pragma unroll 1
-    for (int p = 0; p < NORD; ++p) {
-      double2 v = make_double2(0.0, 0.0);
-      if (take) v = __ldcg(src + t * NORD + p);
-      if (m == 0) {
-        v.x = __shfl_sync(0xffffffffu, v.x, 0);
-        v.y = __shfl_sync(0xffffffffu, v.y, 0);
-      } else {
-        v = warp_sum2(cmul(P.tab_tile[p * kTileTab + lane], v));
-      }
-      if (lane == 0) {
-        const double2 sc = s_scl[p];
-        s_run[p] = cadd(s_run[p], cmul(sc, v));
-        s_scl[p] = cmul(sc, P.tab_tile[p * kTileTab + 32]);
-      }
+    if (lane <= m) {
+      const double2* src = (st == 2) ? P.incl : P.agg;
+#pragma unroll
+      for (int p = 0; p < NORD; ++p)
+        S.pay[lane][p] = (st == 3) ? make_double2(0.0, 0.0) : __ldcg(src + t * NORD + p);
+    }
+    __syncwarp();
+    if (lane < NORD) {
+      // acc = sum_{l<=m} z^{TT l} v_l by Horner from the oldest tile
+      double2 acc = S.pay[m][lane];
+      for (int l = m - 1; l >= 0; --l) acc = cadd(cmul(acc, zT), S.pay[l][lane]);
+      run = cadd(run, cmul(scl, acc));
+      scl = cmul(scl, z32T);
     }
     __syncwarp();
     if (inc) break;
     base -= 32;
   }
-  if (lane < NORD) P.incl[gt * NORD + lane] = cadd(cmul(P.tab_tile[lane * kTileTab + 1], s_run[lane]), s_agg[lane]);
+  if (lane < NORD) {
+    S.carry[lane] = run;
+    P.incl[gt * NORD + lane] = cadd(cmul(zT, run), S.tagg[lane]);
+  }
   __syncwarp();
   if (lane == 0) {
     __threadfence();
@@ -206,251 +288,380 @@ __device__ __forceinline__ void lookback(const ScanParams<T>& P, long long gt, l
   __syncwarp();
 }
 
-template <typename T, int NORD, int MODE, int L, int NT>
-__global__ void __launch_bounds__(NT) sft_scan_kernel(const __grid_constant__ ScanParams<T> P) {
+// Loads the L lead / trail samples this thread stages for the tile starting at output
+// index o0 (coalesced, element e = tid + k*NT) into registers (prefetch). Interior
+// tiles (both windows inside the signal and past the warm start) skip all checks.
+template <typename T, int L, int NT>
+__device__ __forceinline__ void fetch_tile(const ScanParams<T>& P, const T* __restrict__ xs, long long o0,
+                                           int tid, T (&fl)[L], T (&ft)[L]) {
+  constexpr int TT = NT * L;
+  const long long lead_min = P.lo - P.K;  // virtual zero before the warm start
+  const unsigned long long pol = l2_keep_policy();
+  const long long l0 = P.lo + o0 + P.K, t0 = P.lo + o0 - P.K;
+  if (o0 >= 0 && t0 >= 0 && l0 + TT <= P.n && l0 >= lead_min) {
+    const T* pl = xs + l0 + tid;
+    const T* pt = xs + t0 + tid;
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      fl[k] = ld_keep(pl + k * NT, pol);
+      ft[k] = __ldcs(pt + k * NT);
+    }
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < L; ++k) {
+    const long long o = o0 + tid + k * NT;
+    const long long pos = P.lo + o;
+    const long long jl = pos + P.K;
+    fl[k] = (jl >= lead_min) ? load_ext_keep(xs, P.n, P.boundary, jl, pol) : T(0);
+    ft[k] = (o >= 0) ? load_ext(xs, P.n, P.boundary, pos - P.K) : T(0);
+  }
+}
+
+// Complex arithmetic on the recurrence state. fp32: packed pair {re, im} in one 64-bit
+// register, every complex multiply-add = two FFMA2; fp64: scalar DFMA.
+template <typename T>
+struct Cx;
+
+template <>
+struct Cx<float> {
+  using S = u64;
+  using C = OrdConst<float>;
+  static __device__ __forceinline__ S zero() { return 0ull; }
+  static __device__ __forceinline__ S make(float a, float b) { return pk(a, b); }
+  static __device__ __forceinline__ float re(S v) { return plo(v); }
+  static __device__ __forceinline__ float im(S v) { return phi(v); }
+  // v + w u, w packed as {wr, wr, -wi, wi}
+  static __device__ __forceinline__ S madd(const float* w4, S u, S v) {
+    return fma2(ldp(w4 + 2), pswap(u), fma2(ldp(w4), u, v));
+  }
+  // z V + g, g packed {gr, gi}
+  static __device__ __forceinline__ S step(const C& c, S V, S g) {
+    return fma2(ldp(c.zx), pswap(V), fma2(ldp(c.zz), V, g));
+  }
+  // acc + {k1 Vr + k2 Vi, k3 Vr + k4 Vi}
+  static __device__ __forceinline__ S comb(const C& c, S V, S acc) {
+    return fma2(ldp(c.kb), pk(im(V), im(V)), fma2(ldp(c.ka), pk(re(V), re(V)), acc));
+  }
+  static __device__ __forceinline__ float comb_re(const C& c, S V, float acc) {
+    return fmaf(c.ka[0], re(V), fmaf(c.kb[0], im(V), acc));
+  }
+  // acc + z^{L-1-i} g for real g / complex g = {gr, gi}
+  static __device__ __forceinline__ S agg_r(const C& c, int i, float g, S acc) {
+    return fma2(ldp(&c.w[i][0]), pk(g, g), acc);
+  }
+  static __device__ __forceinline__ S agg_c(const C& c, int i, S g, S acc) {
+    return fma2(ldp(&c.w[i][2]), pk(im(g), im(g)), fma2(ldp(&c.w[i][0]), pk(re(g), re(g)), acc));
+  }
+  static __device__ __forceinline__ S shfl_up(S v, int d) {
+    return pk(__shfl_up_sync(0xffffffffu, re(v), d), __shfl_up_sync(0xffffffffu, im(v), d));
+  }
+};
+
+template <>
+struct Cx<double> {
+  using S = double2;
+  using C = OrdConst<double>;
+  static __device__ __forceinline__ S zero() { return make_double2(0.0, 0.0); }
+  static __device__ __forceinline__ S make(double a, double b) { return make_double2(a, b); }
+  static __device__ __forceinline__ double re(S v) { return v.x; }
+  static __device__ __forceinline__ double im(S v) { return v.y; }
+  static __device__ __forceinline__ S madd(const double* w4, S u, S v) {
+    const double wr = w4[0], wi = w4[3];
+    return make_double2(fma(wr, u.x, fma(-wi, u.y, v.x)), fma(wr, u.y, fma(wi, u.x, v.y)));
+  }
+  static __device__ __forceinline__ S step(const C& c, S V, S g) {
+    const double zr = c.zz[0], zi = c.zx[1];
+    return make_double2(fma(zr, V.x, fma(-zi, V.y, g.x)), fma(zr, V.y, fma(zi, V.x, g.y)));
+  }
+  static __device__ __forceinline__ S comb(const C& c, S V, S acc) {
+    return make_double2(fma(c.ka[0], V.x, fma(c.kb[0], V.y, acc.x)), fma(c.ka[1], V.x, fma(c.kb[1], V.y, acc.y)));
+  }
+  static __device__ __forceinline__ double comb_re(const C& c, S V, double acc) {
+    return fma(c.ka[0], V.x, fma(c.kb[0], V.y, acc));
+  }
+  static __device__ __forceinline__ S agg_r(const C& c, int i, double g, S acc) {
+    return make_double2(fma(c.w[i][0], g, acc.x), fma(c.w[i][1], g, acc.y));
+  }
+  static __device__ __forceinline__ S agg_c(const C& c, int i, S g, S acc) {
+    return make_double2(fma(c.w[i][0], g.x, fma(-c.w[i][1], g.y, acc.x)), fma(c.w[i][1], g.x, fma(c.w[i][0], g.y, acc.y)));
+  }
+  static __device__ __forceinline__ S shfl_up(S v, int d) {
+    return make_double2(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
+  }
+};
+
+// One tile: stage samples, phase 1, scans, carry (SEQ: from smem; LB: look-back),
+// phase 2, stores. `fl/ft` hold this tile's prefetched samples on entry and the next
+// tile's on exit when `has_next`.
+template <typename T, int NORD, int NA, int GM, int MODE, int L, int NT, bool SEQ>
+__device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L, NT>& S, long long sig,
+                                        long long gt, long long first, long long o0, T (&fl)[L], T (&ft)[L],
+                                        const T* __restrict__ xs, bool has_next) {
+  using X = Cx<T>;
+  using St = typename X::S;
   using T2 = typename Vec2<T>::t;
   constexpr int TT = NT * L;
   constexpr int NW = NT / 32;
-  constexpr int LOGNW = NW >= 16 ? 4 : NW >= 8 ? 3 : NW >= 4 ? 2 : NW >= 2 ? 1 : 0;
-  constexpr int PAD = TT + TT / 32;
-  static_assert(NORD >= 1 && NORD <= kMaxOrd, "order count");
-  static_assert(NW <= 16, "at most 16 warps");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool warm = o0 + TT <= 0;
+  // staging buffer parity: alternate per tile so the next tile's stores never race
+  // this tile's reads (buffer b was last read two tiles ago, behind two barriers)
+  const int b = SEQ ? static_cast<int>(((o0 / TT) % 2 + 2) % 2) : 0;
+  T* const sl = S.lead[b];
+  T* const stl = S.trail[b];
 
-  __shared__ T s_lead[PAD];
-  __shared__ T s_trail[PAD];
-  __shared__ T2 s_w[NW][NORD];
-  __shared__ double2 s_lb[3][NORD];  // tile aggregate, carry, scale
-  __shared__ long long s_tile;
-  __shared__ unsigned int s_epoch;
-
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int warp = tid >> 5;
-
-  if (tid == 0) {
-    s_tile = static_cast<long long>(atomicAdd(P.ctrl, 1u));
-    s_epoch = *reinterpret_cast<volatile unsigned int*>(P.ctrl + 2);
-  }
-  __syncthreads();
-  const long long gt = s_tile;
-  const unsigned int epoch = s_epoch;
-  const long long sig = gt / P.tiles_per_signal;
-  const long long first = sig * P.tiles_per_signal;
-  const long long o0 = (gt - first - P.warm_tiles) * TT;  // first output index of this tile
-  const T* __restrict__ xs = P.x + sig * P.ld_x;
-
-  // ---- stage the leading (x[n+K]) and trailing (x[n-K]) samples, coalesced
-  {
-    const long long lead_min = P.lo - P.K;  // virtual zero before the warm start
 #pragma unroll
-    for (int k = 0; k < L; ++k) {
-      const int e = tid + k * NT;
-      const long long o = o0 + e;
-      const long long pos = P.lo + o;
-      const long long jl = pos + P.K;
-      const int se = e + (e >> 5);
-      s_lead[se] = (jl >= lead_min) ? load_ext(xs, P.n, P.boundary, jl) : T(0);
-      s_trail[se] = (o >= 0) ? load_ext(xs, P.n, P.boundary, pos - P.K) : T(0);
-    }
+  for (int k = 0; k < L; ++k) {
+    const int e = tid + k * NT;
+    sl[e + (e >> 5)] = fl[k];
+    stl[e + (e >> 5)] = ft[k];
   }
   __syncthreads();
-  T xl[L], xt[L];
+  if (has_next) fetch_tile<T, L, NT>(P, xs, o0 + TT, tid, fl, ft);  // in flight during this tile
+
+  // ---- injections, shared across orders where the group mode allows
+  T xt_[L];
+  St gA[L];  // {x[n+K] - cA x[n-K], 0}
+  constexpr int LB = GM == kGroupSplit ? L : 1;
+  St gB[LB];  // {x[n+K] - Re(cB) x[n-K], -Im(cB) x[n-K]}
 #pragma unroll
   for (int i = 0; i < L; ++i) {
     const int e = tid * L + i;
-    xl[i] = s_lead[e + (e >> 5)];
-    xt[i] = s_trail[e + (e >> 5)];
+    const T xl = sl[e + (e >> 5)], xt = stl[e + (e >> 5)];
+    xt_[i] = xt;
+    gA[i] = X::make(GM == kGroupPerOrder ? xl : fma(-P.cAr, xt, xl), T(0));
+    if constexpr (GM == kGroupSplit) gB[i] = X::make(fma(-P.cBr, xt, xl), -P.cBi * xt);
   }
+  // Per-order injection (group mode 2) is recomputed in phase 2 from shared memory;
+  // the volatile re-read keeps the compiler from caching NORD*L complex values.
+  auto inj = [&](const OrdConst<T>& c, int p, int i, bool reload) -> St {
+    if (GM == kGroupShared || (GM == kGroupSplit && p < NA)) return gA[i];
+    if constexpr (GM == kGroupSplit) return gB[i];
+    const int e = tid * L + i;
+    const T xl = reload ? *reinterpret_cast<volatile const T*>(sl + e + (e >> 5)) : sl[e + (e >> 5)];
+    const T xt = reload ? *reinterpret_cast<volatile const T*>(stl + e + (e >> 5)) : xt_[i];
+    return X::make(fma(-c.cc[0], xt, xl), -c.cc[1] * xt);
+  };
 
-  // ---- phase 1: per-thread aggregate (zero state in), all orders
-  T2 st[NORD];
+  // ---- phase 1: per-thread aggregate with zero state in
+  St st[NORD];
 #pragma unroll
   for (int p = 0; p < NORD; ++p) {
     const OrdConst<T>& c = P.oc[p];
-    T vr = fma(-c.cr, xt[0], xl[0]);
-    T vi = -c.ci * xt[0];
+    St acc = X::zero();
+    if (GM == kGroupShared || (GM == kGroupSplit && p < NA)) {
 #pragma unroll
-    for (int i = 1; i < L; ++i) {
-      const T gr = fma(-c.cr, xt[i], xl[i]);
-      const T gi = -c.ci * xt[i];
-      const T nr = fma(c.zr, vr, fma(-c.zi, vi, gr));
-      const T ni = fma(c.zr, vi, fma(c.zi, vr, gi));
-      vr = nr;
-      vi = ni;
+      for (int i = 0; i < L; ++i) acc = X::agg_r(c, i, X::re(gA[i]), acc);
+    } else {
+#pragma unroll
+      for (int i = 0; i < L; ++i) acc = X::agg_c(c, i, inj(c, p, i, false), acc);
     }
-    st[p] = make2<T2>(vr, vi);
+    st[p] = acc;
   }
 
-  // ---- warp inclusive scan of (z^{L*d}, state) pairs
+  // ---- warp inclusive scan of (z^{L*d}, state) pairs, then exclusive
 #pragma unroll
   for (int p = 0; p < NORD; ++p) {
-    T2 v = st[p];
-    const T2* tb = P.tab + p * kTabStride;
+    St v = st[p];
+
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
       const int d = 1 << k;
-      const T ur = __shfl_up_sync(0xffffffffu, v.x, d);
-      const T ui = __shfl_up_sync(0xffffffffu, v.y, d);
-      if (lane >= d) {
-        const T2 w = tb[32 + k];
-        v.x = fma(w.x, ur, fma(-w.y, ui, v.x));
-        v.y = fma(w.x, ui, fma(w.y, ur, v.y));
-      }
+      const St u = X::shfl_up(v, d);
+      if (lane >= d) v = X::madd(P.oc[p].scan[k], u, v);
     }
-    st[p] = v;
-  }
-  if (lane == 31) {
-#pragma unroll
-    for (int p = 0; p < NORD; ++p) s_w[warp][p] = st[p];
-  }
-#pragma unroll
-  for (int p = 0; p < NORD; ++p) {  // inclusive -> exclusive within the warp
-    const T ur = __shfl_up_sync(0xffffffffu, st[p].x, 1);
-    const T ui = __shfl_up_sync(0xffffffffu, st[p].y, 1);
-    st[p] = lane ? make2<T2>(ur, ui) : make2<T2>(T(0), T(0));
+    if (lane == 31) S.w[warp][p] = make2<T2>(X::re(v), X::im(v));
+    const St u = X::shfl_up(v, 1);
+    st[p] = lane ? u : X::zero();
   }
   __syncthreads();
 
-  // ---- warp 0: inter-warp scan, tile aggregate, look-back, per-warp carries
-  if (warp == 0) {
-#pragma unroll 1
-    for (int p = 0; p < NORD; ++p) {
-      const T2* tb = P.tab + p * kTabStride;
-      T2 v = lane < NW ? s_w[lane][p] : make2<T2>(T(0), T(0));
+  // ---- one thread per order: inter-warp scan, tile aggregate, carry, per-warp carries
+  if (tid < NORD) {
+    const int p = tid;
+
+    St ex[NW];
+    St run = X::zero();
 #pragma unroll
-      for (int k = 0; k < LOGNW; ++k) {
-        const int d = 1 << k;
-        const T ur = __shfl_up_sync(0xffffffffu, v.x, d);
-        const T ui = __shfl_up_sync(0xffffffffu, v.y, d);
-        if (lane >= d) {
-          const T2 w = tb[56 + k];
-          v.x = fma(w.x, ur, fma(-w.y, ui, v.x));
-          v.y = fma(w.x, ui, fma(w.y, ur, v.y));
+    for (int w = 0; w < NW; ++w) {
+      ex[w] = run;
+      const T2 t = S.w[w][p];
+      run = X::madd(P.oc[p].m32, run, X::make(t.x, t.y));  // z^{32L} run + total_w
+    }
+    S.tagg[p] = make_double2(static_cast<double>(X::re(run)), static_cast<double>(X::im(run)));
+    if constexpr (SEQ) {
+      const double2 c = S.carry[p];
+      const St cs = X::make(static_cast<T>(c.x), static_cast<T>(c.y));
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const St r = X::madd(P.oc[p].wrot[w], cs, ex[w]);
+        S.w[w][p] = make2<T2>(X::re(r), X::im(r));
+      }
+      S.carry[p] = cadd(cmul(P.tab_tile[p * 2], c), S.tagg[p]);
+    } else {
+#pragma unroll
+      for (int w = 0; w < NW; ++w) S.w[w][p] = make2<T2>(X::re(ex[w]), X::im(ex[w]));
+    }
+  }
+  if constexpr (!SEQ) {
+    if (warp == 0) {
+      __syncwarp();
+      lookback<T, NORD, L, NT>(P, S, gt, first, lane);
+      if (tid < NORD) {
+        const int p = tid;
+
+        const St cs = X::make(static_cast<T>(S.carry[p].x), static_cast<T>(S.carry[p].y));
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const T2 e = S.w[w][p];
+          const St r = X::madd(P.oc[p].wrot[w], cs, X::make(e.x, e.y));
+          S.w[w][p] = make2<T2>(X::re(r), X::im(r));
         }
       }
-      const T ur = __shfl_up_sync(0xffffffffu, v.x, 1);
-      const T ui = __shfl_up_sync(0xffffffffu, v.y, 1);
-      if (lane < NW) s_w[lane][p] = lane ? make2<T2>(ur, ui) : make2<T2>(T(0), T(0));  // exclusive
-      if (lane == NW - 1) s_lb[0][p] = make_double2(static_cast<double>(v.x), static_cast<double>(v.y));
-    }
-    __syncwarp();
-    lookback<T, NORD>(P, gt, first, epoch, s_lb[0], s_lb[1], s_lb[2], lane);
-    if (lane < NW) {
-#pragma unroll 1
-      for (int p = 0; p < NORD; ++p) {
-        const T2 w = P.tab[p * kTabStride + 40 + lane];
-        const T cr = static_cast<T>(s_lb[1][p].x), ci = static_cast<T>(s_lb[1][p].y);
-        const T2 ex = s_w[lane][p];
-        s_w[lane][p] = make2<T2>(fma(w.x, cr, fma(-w.y, ci, ex.x)), fma(w.x, ci, fma(w.y, cr, ex.y)));
-      }
     }
   }
   __syncthreads();
-  if (tid == 0) {
-    // every CTA has its ticket and has finished its look-back: the last one re-arms
-    __threadfence();
-    if (atomicAdd(P.ctrl + 1, 1u) == static_cast<unsigned int>(P.total_tiles - 1)) {
-      atomicExch(P.ctrl, 0u);
-      atomicExch(P.ctrl + 1, 0u);
-      atomicAdd(P.ctrl + 2, 1u);
+  if constexpr (!SEQ) {
+    if (tid == 0) {
+      // every CTA of the launch has its ticket and its look-back done: the last re-arms
       __threadfence();
+      if (atomicAdd(P.ctrl + 1, 1u) == static_cast<unsigned int>(P.total_tiles - 1)) {
+        atomicExch(P.ctrl, 0u);
+        atomicExch(P.ctrl + 1, 0u);
+        atomicAdd(P.ctrl + 2, 1u);
+        __threadfence();
+      }
     }
   }
-
-  if (o0 + TT <= 0) return;  // warm tile: no outputs
+  if (warm) return;  // warm tile: phase 1 only (uniform per CTA)
 
   // state entering this thread's segment: z^{L*lane} * Cw + in-warp exclusive
 #pragma unroll
   for (int p = 0; p < NORD; ++p) {
-    const T2 cw = s_w[warp][p];
-    const T2 w = P.tab[p * kTabStride + lane];
-    st[p] = make2<T2>(fma(w.x, cw.x, fma(-w.y, cw.y, st[p].x)), fma(w.x, cw.y, fma(w.y, cw.x, st[p].y)));
+    const T2 cw = S.w[warp][p];
+    st[p] = X::madd(P.tab + (p * kTabStride + lane) * 4, X::make(cw.x, cw.y), st[p]);
   }
 
-  const long long ob = o0 + static_cast<long long>(tid) * L;  // first output of this thread
-  if (ob >= P.count) return;
-  const bool full = ob >= 0 && ob + L <= P.count;
-
+  // ---- phase 2: re-run the recurrence from the true state and combine
+  const long long ob = o0 + static_cast<long long>(tid) * L;
   if constexpr (MODE == kModeComps) {
 #pragma unroll
     for (int p = 0; p < NORD; ++p) {
       const OrdConst<T>& c = P.oc[p];
-      T vr = st[p].x, vi = st[p].y;
+      St v = st[p];
       T* cptr = P.out + p * P.ord_stride + sig * P.ld_out;
       T* sptr = P.out_s + p * P.ord_stride + sig * P.ld_out;
 #pragma unroll
       for (int i = 0; i < L; ++i) {
-        const T gr = fma(-c.cr, xt[i], xl[i]);
-        const T gi = -c.ci * xt[i];
-        const T nr = fma(c.zr, vr, fma(-c.zi, vi, gr));
-        const T ni = fma(c.zr, vi, fma(c.zi, vr, gi));
-        vr = nr;
-        vi = ni;
+        v = X::step(c, v, inj(c, p, i, true));
         const long long o = ob + i;
-        if (o >= 0 && o < P.count) {
-          cptr[o] = fma(c.k1, vr, fma(-c.k2, vi, c.k3 * xt[i]));
-          sptr[o] = -fma(c.k2, vr, fma(c.k1, vi, c.k4 * xt[i]));
+        if (o < P.count) {
+          // c = Re(a V + b x_t), s = -Im(a V + b x_t), a = (k1, k2), b = (k3, k4) = (ka[1], kb[1])
+          const T vr = X::re(v), vi = X::im(v), xt = xt_[i];
+          cptr[o] = fma(c.ka[0], vr, fma(-c.kb[0], vi, c.ka[1] * xt));
+          sptr[o] = -fma(c.kb[0], vr, fma(c.ka[0], vi, c.kb[1] * xt));
         }
       }
     }
   } else {
     constexpr bool CPLX = MODE == kModeComplex;
-    T ar[L], ai[L];
+    St acc[CPLX ? L : 1];
+    T accr[CPLX ? 1 : L];
 #pragma unroll
     for (int i = 0; i < L; ++i) {
-      ar[i] = P.Dr * xt[i];
-      ai[i] = CPLX ? P.Di * xt[i] : T(0);
+      if constexpr (CPLX)
+        acc[i] = X::make(P.Dr * xt_[i], P.Di * xt_[i]);
+      else
+        accr[i] = P.Dr * xt_[i];
     }
 #pragma unroll
     for (int p = 0; p < NORD; ++p) {
       const OrdConst<T>& c = P.oc[p];
-      T vr = st[p].x, vi = st[p].y;
+      St v = st[p];
 #pragma unroll
       for (int i = 0; i < L; ++i) {
-        const T gr = fma(-c.cr, xt[i], xl[i]);
-        const T gi = -c.ci * xt[i];
-        const T nr = fma(c.zr, vr, fma(-c.zi, vi, gr));
-        const T ni = fma(c.zr, vi, fma(c.zi, vr, gi));
-        vr = nr;
-        vi = ni;
-        ar[i] = fma(c.k1, vr, fma(c.k2, vi, ar[i]));
-        if (CPLX) ai[i] = fma(c.k3, vr, fma(c.k4, vi, ai[i]));
+        v = X::step(c, v, inj(c, p, i, true));
+        if constexpr (CPLX)
+          acc[i] = X::comb(c, v, acc[i]);
+        else
+          accr[i] = X::comb_re(c, v, accr[i]);
       }
     }
-    if (CPLX) {
-      T* optr = P.out + 2 * (sig * P.ld_out);
-      if (full && P.vec_ok && !P.accumulate) {
-        T2* o2 = reinterpret_cast<T2*>(optr) + ob;
+    // ---- stores: L consecutive outputs per thread, 16-byte vectors when aligned
+    constexpr int CW = CPLX ? 2 : 1;  // T words per output
+    T buf[L * CW];
 #pragma unroll
-        for (int i = 0; i < L; ++i) o2[i] = make2<T2>(ar[i], ai[i]);
+    for (int i = 0; i < L; ++i) {
+      if constexpr (CPLX) {
+        buf[2 * i] = X::re(acc[i]);
+        buf[2 * i + 1] = X::im(acc[i]);
       } else {
+        buf[i] = accr[i];
+      }
+    }
+    T* optr = P.out + CW * (sig * P.ld_out);
+    constexpr int VW = 16 / sizeof(T);  // T words per 16-byte vector
+    if (P.vec_ok && !P.accumulate && ob + L <= P.count && (L * CW) % VW == 0) {
+      T* dst = optr + ob * CW;
 #pragma unroll
-        for (int i = 0; i < L; ++i) {
-          const long long o = ob + i;
-          if (o >= 0 && o < P.count) {
-            if (P.accumulate) {
-              optr[2 * o] += ar[i];
-              optr[2 * o + 1] += ai[i];
-            } else {
-              optr[2 * o] = ar[i];
-              optr[2 * o + 1] = ai[i];
-            }
-          }
-        }
+      for (int v = 0; v < L * CW / VW; ++v) {
+        if constexpr (sizeof(T) == 4)
+          __stcs(reinterpret_cast<float4*>(dst) + v,
+                 make_float4(buf[v * 4], buf[v * 4 + 1], buf[v * 4 + 2], buf[v * 4 + 3]));
+        else
+          __stcs(reinterpret_cast<double2*>(dst) + v, make_double2(buf[v * 2], buf[v * 2 + 1]));
       }
     } else {
-      T* optr = P.out + sig * P.ld_out;
 #pragma unroll
       for (int i = 0; i < L; ++i) {
         const long long o = ob + i;
-        if (o >= 0 && o < P.count) {
-          if (P.accumulate)
-            optr[o] += ar[i];
-          else
-            optr[o] = ar[i];
+        if (o < P.count) {
+#pragma unroll
+          for (int w = 0; w < CW; ++w) {
+            if (P.accumulate)
+              optr[o * CW + w] += buf[i * CW + w];
+            else
+              optr[o * CW + w] = buf[i * CW + w];
+          }
         }
       }
     }
+  }
+}
+
+template <typename T, int NORD, int NA, int GM, int MODE, int L, int NT, bool SEQ>
+__global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? 4 : 2)) sft_scan_kernel(const __grid_constant__ ScanParams<T> P) {
+  static_assert(NORD >= 1 && NORD <= kMaxOrd, "order count");
+  static_assert(L <= kMaxL, "positions per thread");
+  constexpr int TT = NT * L;
+  __shared__ Smem<T, NORD, L, NT> S;
+  const int tid = threadIdx.x;
+  T fl[L], ft[L];
+
+  if constexpr (SEQ) {
+    // one CTA per signal, tiles in order, carry in shared memory
+    const long long sig = blockIdx.x;
+    const T* __restrict__ xs = P.x + sig * P.ld_x;
+    if (tid < NORD) S.carry[tid] = make_double2(0.0, 0.0);
+    const long long o_first = -P.warm_tiles * TT;
+    fetch_tile<T, L, NT>(P, xs, o_first, tid, fl, ft);
+    for (long long t = 0; t < P.tiles_per_signal; ++t)
+      do_tile<T, NORD, NA, GM, MODE, L, NT, true>(P, S, sig, 0, 0, o_first + t * TT, fl, ft, xs,
+                                              t + 1 < P.tiles_per_signal);
+  } else {
+    if (tid == 0) {
+      S.tile = static_cast<long long>(atomicAdd(P.ctrl, 1u));
+      S.epoch = *reinterpret_cast<volatile unsigned int*>(P.ctrl + 2);
+    }
+    __syncthreads();
+    const long long gt = S.tile;
+    const long long sig = gt / P.tiles_per_signal;
+    const long long first = sig * P.tiles_per_signal;
+    const long long o0 = (gt - first - P.warm_tiles) * TT;
+    const T* __restrict__ xs = P.x + sig * P.ld_x;
+    fetch_tile<T, L, NT>(P, xs, o0, tid, fl, ft);
+    do_tile<T, NORD, NA, GM, MODE, L, NT, false>(P, S, sig, gt, first, o0, fl, ft, xs, false);
   }
 }
 

@@ -86,6 +86,7 @@ struct Lowered {
 // Group of <= kMaxOrd orders executed by one kernel launch.
 struct Group {
   int nord = 0;
+  int gm = sftk::kGroupPerOrder;
   sftk::ScanParams<float> pf{};
   sftk::ScanParams<double> pd{};
   void* d_tab = nullptr;
@@ -101,7 +102,8 @@ struct sftgpu_plan {
   int conv = 0;  // GCT3/MCT3 direct convolution plan
   long long n = 0, batch = 0, lo = 0, count = 0;
   int K = 1, boundary = SFTGPU_BOUNDARY_CLAMP;
-  int L = 4, NT = 256;
+  int L = 8, NT = 128;
+  int seq = 0;  // 1: one CTA walks a whole signal (batched), no look-back workspace
   long long TT = 1024, tiles_per_signal = 0, warm_tiles = 0, total_tiles = 0;
   std::vector<Group> groups;
   int max_nord = 1;
@@ -141,19 +143,65 @@ size_t elem_size(int precision) { return precision == SFTGPU_SINGLE ? sizeof(flo
 
 // ---------------------------------------------------------------- kernel dispatch
 template <typename T>
-void launch_scan(int L, int nord, int mode, const sftk::ScanParams<T>& p, long long grid, cudaStream_t s) {
-  if (nord < 1 || nord > sftk::kMaxOrd) fail(SFTGPU_EINTERNAL, "order group size out of range");
-  switch (mode) {
-    case sftk::kModeReal: sftk::launch_scan<T, sftk::kModeReal>(L, nord, p, grid, s); break;
-    case sftk::kModeComplex: sftk::launch_scan<T, sftk::kModeComplex>(L, nord, p, grid, s); break;
-    default: sftk::launch_scan<T, sftk::kModeComps>(L, nord, p, grid, s); break;
+void launch_scan(const sftgpu_plan* pl, const Group& g, const sftk::ScanParams<T>& p, cudaStream_t s) {
+  if (g.nord < 1 || g.nord > sftk::kMaxOrd) fail(SFTGPU_EINTERNAL, "order group size out of range");
+  const long long grid = pl->seq ? pl->batch : pl->total_tiles;
+  const sftk::LaunchKey key{g.nord, g.gm, pl->mode, pl->seq};
+  switch (pl->mode) {
+    case sftk::kModeReal:
+      pl->seq ? sftk::launch_scan<T, sftk::kModeReal, true>(key, p, grid, s)
+              : sftk::launch_scan<T, sftk::kModeReal, false>(key, p, grid, s);
+      break;
+    case sftk::kModeComplex:
+      pl->seq ? sftk::launch_scan<T, sftk::kModeComplex, true>(key, p, grid, s)
+              : sftk::launch_scan<T, sftk::kModeComplex, false>(key, p, grid, s);
+      break;
+    default: sftk::launch_scan<T, sftk::kModeComps, false>(key, p, grid, s); break;
   }
 }
 
 // ---------------------------------------------------------------- plan building
+// Orders whose trailing-sample injection constants z^{2K} coincide share one g per
+// position. Returns the group mode and reorders `ords` so the real-shared group comes
+// first (na orders), followed by the complex-shared group.
+int detect_groups(std::vector<Order>& ords, double alpha, int K, cd* cA, cd* cB, int* na) {
+  auto cinj = [&](const Order& o) { return zpow(alpha, o.omega, 2.0 * K); };
+  auto same = [](cd a, cd b) { return std::abs(a - b) <= 1e-13 * std::max(1.0, std::abs(a)); };
+  auto is_real = [](cd a) { return std::abs(a.imag()) <= 1e-13 * std::max(1.0, std::abs(a)); };
+  std::vector<cd> reps;
+  for (const Order& o : ords) {
+    const cd c = cinj(o);
+    bool found = false;
+    for (const cd& r : reps) found = found || same(r, c);
+    if (!found) reps.push_back(c);
+  }
+  if (reps.size() == 1 && is_real(reps[0])) {
+    *cA = cd(reps[0].real(), 0.0);
+    *na = static_cast<int>(ords.size());
+    return sftk::kGroupShared;
+  }
+  if (reps.size() <= 2) {
+    int ireal = -1;
+    for (size_t i = 0; i < reps.size(); ++i)
+      if (is_real(reps[i])) ireal = static_cast<int>(i);
+    if (reps.size() == 1 || ireal >= 0) {
+      const cd a = ireal >= 0 ? cd(reps[ireal].real(), 0.0) : cd(0.0, 0.0);
+      const cd b = reps.size() == 1 ? reps[0] : reps[1 - ireal];
+      std::stable_partition(ords.begin(), ords.end(), [&](const Order& o) { return ireal >= 0 && same(cinj(o), a); });
+      *na = 0;
+      for (const Order& o : ords) *na += (ireal >= 0 && same(cinj(o), a)) ? 1 : 0;
+      *cA = a;
+      *cB = b;
+      return sftk::kGroupSplit;
+    }
+  }
+  *na = 0;
+  return sftk::kGroupPerOrder;
+}
+
 template <typename T>
 void fill_consts(sftk::ScanParams<T>& P, const std::vector<Order>& ords, double alpha, double pref,
-                 int K, bool comps, double* Dr, double* Di) {
+                 int K, int L, bool comps, double* Dr, double* Di) {
   cd D(0.0, 0.0);
   for (size_t i = 0; i < ords.size(); ++i) {
     const double w = ords[i].omega;
@@ -179,14 +227,34 @@ void fill_consts(sftk::ScanParams<T>& P, const std::vector<Order>& ords, double 
       if (!std::isfinite(static_cast<double>(static_cast<T>(v))))
         fail(SFTGPU_EINVAL, "attenuation alpha*K too large for the requested precision");
     sftk::OrdConst<T>& o = P.oc[i];
-    o.zr = static_cast<T>(z.real());
-    o.zi = static_cast<T>(z.imag());
-    o.cr = static_cast<T>(c.real());
-    o.ci = static_cast<T>(c.imag());
-    o.k1 = static_cast<T>(k[0]);
-    o.k2 = static_cast<T>(k[1]);
-    o.k3 = static_cast<T>(k[2]);
-    o.k4 = static_cast<T>(k[3]);
+    const T zr = static_cast<T>(z.real()), zi = static_cast<T>(z.imag());
+    o.zz[0] = zr;
+    o.zz[1] = zr;
+    o.zx[0] = -zi;
+    o.zx[1] = zi;
+    o.ka[0] = static_cast<T>(k[0]);
+    o.ka[1] = static_cast<T>(k[2]);
+    o.kb[0] = static_cast<T>(k[1]);
+    o.kb[1] = static_cast<T>(k[3]);
+    o.cc[0] = static_cast<T>(c.real());
+    o.cc[1] = static_cast<T>(c.imag());
+    auto put4 = [](T* d, cd v) {  // {re, re, -im, im}
+      d[0] = static_cast<T>(v.real());
+      d[1] = static_cast<T>(v.real());
+      d[2] = static_cast<T>(-v.imag());
+      d[3] = static_cast<T>(v.imag());
+    };
+    for (int k2 = 0; k2 < 5; ++k2) put4(o.scan[k2], zpow(alpha, w, static_cast<double>(L) * (1 << k2)));
+    for (int wi = 0; wi < 4; ++wi) put4(o.wrot[wi], zpow(alpha, w, 32.0 * L * wi));
+    put4(o.m32, zpow(alpha, w, 32.0 * L));
+    for (int j = 0; j < L; ++j) {
+      const cd wj = zpow(alpha, w, static_cast<double>(L - 1 - j));
+      const T wr = static_cast<T>(wj.real()), wi = static_cast<T>(wj.imag());
+      o.w[j][0] = wr;
+      o.w[j][1] = wi;
+      o.w[j][2] = -wi;
+      o.w[j][3] = wr;
+    }
   }
   *Dr = D.real();
   *Di = D.imag();
@@ -194,29 +262,30 @@ void fill_consts(sftk::ScanParams<T>& P, const std::vector<Order>& ords, double 
 
 template <typename T>
 void build_tables(Group& g, const std::vector<Order>& ords, double alpha, int L, int NT) {
-  using T2 = typename sftk::Vec2<T>::t;
   const int NW = NT / 32;
   const long long TT = static_cast<long long>(L) * NT;
-  std::vector<T2> tab(static_cast<size_t>(ords.size()) * sftk::kTabStride);
-  std::vector<double2> tt(static_cast<size_t>(ords.size()) * sftk::kTileTab);
-  auto put = [](T2& d, cd v) {
-    d.x = static_cast<T>(v.real());
-    d.y = static_cast<T>(v.imag());
+  std::vector<T> tab(static_cast<size_t>(ords.size()) * sftk::kTabStride * 4, T(0));
+  std::vector<double2> tt(static_cast<size_t>(ords.size()) * 2);
+  auto put = [](T* d, cd v) {  // {re, re, -im, im}
+    d[0] = static_cast<T>(v.real());
+    d[1] = static_cast<T>(v.real());
+    d[2] = static_cast<T>(-v.imag());
+    d[3] = static_cast<T>(v.imag());
   };
   for (size_t p = 0; p < ords.size(); ++p) {
     const double w = ords[p].omega;
-    T2* t = &tab[p * sftk::kTabStride];
-    for (int lane = 0; lane < 32; ++lane) put(t[lane], zpow(alpha, w, static_cast<double>(L) * lane));
-    for (int k = 0; k < 5; ++k) put(t[32 + k], zpow(alpha, w, static_cast<double>(L) * (1 << k)));
-    for (int wi = 0; wi < NW; ++wi) put(t[40 + wi], zpow(alpha, w, 32.0 * L * wi));
-    for (int k = 0; k < 4; ++k) put(t[56 + k], zpow(alpha, w, 32.0 * L * (1 << k)));
-    for (int l = 0; l < sftk::kTileTab; ++l) {
-      const cd v = zpow(alpha, w, static_cast<double>(TT) * l);
-      tt[p * sftk::kTileTab + l] = make_double2(v.real(), v.imag());
+    T* t = &tab[p * sftk::kTabStride * 4];
+    for (int lane = 0; lane < 32; ++lane) put(t + lane * 4, zpow(alpha, w, static_cast<double>(L) * lane));
+    for (int k = 0; k < 5; ++k) put(t + (32 + k) * 4, zpow(alpha, w, static_cast<double>(L) * (1 << k)));
+    for (int wi = 0; wi < NW; ++wi) put(t + (40 + wi) * 4, zpow(alpha, w, 32.0 * L * wi));
+    for (int k = 0; k < 4; ++k) put(t + (56 + k) * 4, zpow(alpha, w, 32.0 * L * (1 << k)));
+    for (int l = 0; l < 2; ++l) {
+      const cd v = zpow(alpha, w, static_cast<double>(TT) * (l == 0 ? 1 : 32));
+      tt[p * 2 + l] = make_double2(v.real(), v.imag());
     }
   }
-  cuda_check(cudaMalloc(&g.d_tab, tab.size() * sizeof(T2)), "cudaMalloc tables");
-  cuda_check(cudaMemcpy(g.d_tab, tab.data(), tab.size() * sizeof(T2), cudaMemcpyHostToDevice), "copy tables");
+  cuda_check(cudaMalloc(&g.d_tab, tab.size() * sizeof(T)), "cudaMalloc tables");
+  cuda_check(cudaMemcpy(g.d_tab, tab.data(), tab.size() * sizeof(T), cudaMemcpyHostToDevice), "copy tables");
   cuda_check(cudaMalloc(&g.d_tab_tile, tt.size() * sizeof(double2)), "cudaMalloc tile tables");
   cuda_check(cudaMemcpy(g.d_tab_tile, tt.data(), tt.size() * sizeof(double2), cudaMemcpyHostToDevice),
              "copy tile tables");
@@ -234,7 +303,7 @@ sftk::ScanParams<double>& params_of<double>(Group& g) {
 }
 
 template <typename T>
-void build_groups(sftgpu_plan* pl, const std::vector<Order>& ords, double alpha, double pref, bool comps) {
+void build_groups(sftgpu_plan* pl, std::vector<Order> ords, double alpha, double pref, bool comps) {
   for (size_t g0 = 0; g0 < ords.size(); g0 += sftk::kMaxOrd) {
     const size_t g1 = std::min(ords.size(), g0 + sftk::kMaxOrd);
     std::vector<Order> sub(ords.begin() + g0, ords.begin() + g1);
@@ -243,29 +312,46 @@ void build_groups(sftgpu_plan* pl, const std::vector<Order>& ords, double alpha,
     g.nord = static_cast<int>(sub.size());
     sftk::ScanParams<T>& P = params_of<T>(g);
     std::memset(&P, 0, sizeof(P));
+    cd cA(0, 0), cB(0, 0);
+    int na = 0;
+    // components keep their order (outputs are per order); transforms may regroup
+    g.gm = comps ? sftk::kGroupPerOrder : detect_groups(sub, alpha, pl->K, &cA, &cB, &na);
+    if (g.gm == sftk::kGroupSplit && (pl->mode != sftk::kModeComplex || sftk::split_na(g.nord) != na))
+      g.gm = sftk::kGroupPerOrder;  // only the multiplication-method layout has a split kernel
+    if (comps) {
+      std::vector<Order> probe = sub;
+      cd a2, b2;
+      int n2;
+      if (detect_groups(probe, alpha, pl->K, &a2, &b2, &n2) == sftk::kGroupShared) {
+        g.gm = sftk::kGroupShared;
+        cA = a2;
+        na = n2;
+      }
+    }
+    P.cAr = static_cast<T>(cA.real());
+    P.cAi = static_cast<T>(cA.imag());
+    P.cBr = static_cast<T>(cB.real());
+    P.cBi = static_cast<T>(cB.imag());
+    P.na = na;
     double Dr = 0, Di = 0;
-    fill_consts<T>(P, sub, alpha, pref, pl->K, comps, &Dr, &Di);
+    fill_consts<T>(P, sub, alpha, pref, pl->K, pl->L, comps, &Dr, &Di);
     P.Dr = g0 == 0 ? static_cast<T>(Dr) : T(0);
     P.Di = g0 == 0 ? static_cast<T>(Di) : T(0);
     build_tables<T>(g, sub, alpha, pl->L, pl->NT);
-    P.tab = static_cast<const typename sftk::Vec2<T>::t*>(g.d_tab);
+    P.tab = static_cast<const T*>(g.d_tab);
     P.tab_tile = g.d_tab_tile;
   }
   pl->max_nord = 1;
   for (const Group& g : pl->groups) pl->max_nord = std::max(pl->max_nord, g.nord);
 }
 
+// SEQ (one CTA per signal) when the batch alone fills the GPU; LB (one tile per CTA
+// with look-back) otherwise. Tile geometry per mode/precision (sftk::Geometry).
 void choose_geometry(sftgpu_plan* pl) {
-  pl->NT = 256;
-  if (pl->precision == SFTGPU_DOUBLE) {
-    pl->L = 4;
-  } else {
-    // prefer 2048-position tiles; fall back to 1024 when that leaves SMs idle
-    pl->L = 8;
-    const long long TT8 = 8LL * pl->NT;
-    const long long tiles8 = (2LL * pl->K + TT8 - 1) / TT8 + (pl->count + TT8 - 1) / TT8;
-    if (pl->batch * tiles8 < 2 * 148) pl->L = 4;
-  }
+  pl->seq = (!pl->is_components && pl->batch >= 256) ? 1 : 0;
+  const bool dbl = pl->precision == SFTGPU_DOUBLE;
+  pl->NT = sftk::kThreads;
+  pl->L = pl->seq ? (dbl ? sftk::kLSeqF64 : sftk::kLSeqF32) : (dbl ? sftk::kLLbF64 : sftk::kLLbF32);
   pl->TT = static_cast<long long>(pl->L) * pl->NT;
   pl->warm_tiles = (2LL * pl->K + pl->TT - 1) / pl->TT;
   pl->tiles_per_signal = pl->warm_tiles + (pl->count + pl->TT - 1) / pl->TT;
@@ -273,6 +359,7 @@ void choose_geometry(sftgpu_plan* pl) {
 }
 
 void alloc_workspace(sftgpu_plan* pl) {
+  if (pl->seq) return;  // SEQ mode needs no inter-CTA state
   if (pl->total_tiles >= (1LL << 31)) fail(SFTGPU_EINVAL, "problem too large for one plan (tiles >= 2^31)");
   const unsigned int ctrl0[4] = {0u, 0u, 1u, 0u};  // epoch starts at 1: zeroed flags are stale
   cuda_check(cudaMalloc(&pl->d_ctrl, sizeof(ctrl0)), "cudaMalloc ctrl");
@@ -531,7 +618,10 @@ void run_groups(sftgpu_plan* pl, const void* x, long long ld_x, void* out, void*
     P.K = pl->K;
     P.boundary = pl->boundary;
     P.accumulate = (gi > 0 && !pl->is_components) ? 1 : accumulate_first;
-    P.vec_ok = (reinterpret_cast<uintptr_t>(out) % (2 * sizeof(T)) == 0) ? 1 : 0;
+    {
+      const size_t rowb = static_cast<size_t>(ld_out) * sizeof(T) * (pl->mode == sftk::kModeComplex ? 2 : 1);
+      P.vec_ok = (reinterpret_cast<uintptr_t>(out) % 16 == 0 && rowb % 16 == 0) ? 1 : 0;
+    }
     P.tiles_per_signal = pl->tiles_per_signal;
     P.warm_tiles = pl->warm_tiles;
     P.total_tiles = pl->total_tiles;
@@ -546,7 +636,7 @@ void run_groups(sftgpu_plan* pl, const void* x, long long ld_x, void* out, void*
       P.out = static_cast<T*>(out) + skip * P.ord_stride;
       P.out_s = static_cast<T*>(out_s) + skip * P.ord_stride;
     }
-    launch_scan<T>(pl->L, g.nord, pl->mode, P, pl->total_tiles, st);
+    launch_scan<T>(pl, g, P, st);
     cuda_check(cudaGetLastError(), "sft_scan_kernel launch");
   }
 }

@@ -307,3 +307,32 @@ def test_gpu_truncated_convolution_matches_oracle(sft, O):
         got = sft.truncated_convolution(sft.Signal(x, boundary), sft.KernelTaps(taps, -700))
         ref = O.truncated_convolution(x, boundary, taps, -700, 8)
         assert rel_max(got, ref) < 1e-13
+
+
+@pytest.mark.parametrize("abbrev,sigma,xi,prec,tol", [("MMS5P3", 64.0, 10.0, 0, 1e-5), ("GDP6", 100.0, 0.0, 1, 1e-12),
+                                                      ("MDS3P6", 40.0, 8.0, 0, 1e-5), ("MMP2", 30.0, 4.0, 1, 1e-12)])
+def test_batched_seq_mode_vs_oracle(sft, O, abbrev, sigma, xi, prec, tol):
+    """Batches >= 256 signals run one CTA per signal (SEQ mode, no look-back): rows are
+    checked against the oracle, and every row against the single-signal (LB) result."""
+    import torch
+
+    spec = sft.make_transform_spec(abbrev, sigma, xi, sft.TransformOptions(precision=prec))
+    B, n = 300, 3001
+    xb = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 99, B, sft.Precision(prec))
+    plan = sft.TransformPlan(spec, n, B)
+    out = plan.empty_output()
+    plan.execute(xb, out)
+    torch.cuda.synchronize()
+    xh = xb.double().cpu().numpy()
+    oh = out.double().cpu().numpy()
+    vals = oh[..., 0] + 1j * oh[..., 1] if plan.complex_out else oh
+    for b in (0, 137, 299):
+        assert rel_max(vals[b], oracle_transform(O, xh[b], 1, spec)) < tol
+    single = sft.TransformPlan(spec, n, 1)
+    o1 = single.empty_output()
+    for b in (5, 250):
+        single.execute(xb[b:b + 1].contiguous(), o1)
+        torch.cuda.synchronize()
+        r = o1.double().cpu().numpy()[0]
+        r = r[..., 0] + 1j * r[..., 1] if plan.complex_out else r
+        assert rel_max(vals[b], r) < tol
