@@ -326,18 +326,132 @@ def run_ours(args, w, spec_of):
         dist.destroy_process_group()
 
 
+def run_scalogram(args):
+    """BASELINE config 5: 128-scale Morlet scalogram (direct, P_D=6, xi=10) on N=2^24,
+    scales sharded across ranks, input broadcast once (NCCL), gather timed separately."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2110_11866_b200 as P
+    from paper_2110_11866_b200 import scalogram as SG
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, ns = args.scalogram_n, args.scalogram_scales
+    cache = os.path.join(ROOT, "paper_2110_11866_b200", "data", f"scalogram{ns}_xi10_pd6.coef")
+    specs = SG.build_specs(SG.scale_sigmas(ns), xi=10.0, pd=6, cache=cache)
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    if rank == 0:
+        x.copy_(P.generate_signals(P.TestSignalKind.SeededNoise, n, 1234, 1, P.Precision.Single)[0])
+    if world > 1:
+        dist.broadcast(x, src=0)
+    sc = SG.Scalogram(n, specs, world, rank, args.shard)
+    out = sc.empty_output()
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            sc.run(x, out)
+        stream.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            for _ in range(args.steps):
+                sc.run(x, out)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+        ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = n * ns * args.steps / (ms * 1e-3) / 1e6
+    # final gather to rank 0 (optional, timed separately)
+    gather_ms = None
+    if world > 1 and args.gather:
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0 = time.perf_counter()
+        sc.gather(out)
+        torch.cuda.synchronize()
+        gather_ms = (time.perf_counter() - g0) * 1e3
+    # e2e: pinned host input -> H2D, all of this rank's scales, D2H of its rows
+    xh = torch.empty(n, dtype=torch.float32).pin_memory()
+    xh.copy_(x.cpu())
+    oh = torch.empty(out.shape, dtype=torch.float32).pin_memory()
+    if world > 1:
+        dist.barrier()
+    e0 = time.perf_counter()
+    with torch.cuda.stream(stream):
+        xd = torch.empty_like(x)
+        xd.copy_(xh, non_blocking=True)
+        sc.run(xd, out)
+        oh.copy_(out, non_blocking=True)
+        stream.synchronize()
+    te = torch.tensor([time.perf_counter() - e0], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = n * ns / float(te.item()) / 1e6
+    peak, peak_src = measured_peaks()
+    launches_per_step = sc.launches
+    kernel_ms = ms / args.steps / max(1, launches_per_step)
+    step_bytes = len(sc.rows) * sc.count * 12
+    achieved = step_bytes / max(1, launches_per_step) / (kernel_ms * 1e-3) / 1e9
+    if rank == 0:
+        line = {
+            "metric": "Morlet transform ms @N=102400,σ=8192; Msamples·scales/s; HBM GB/s vs peak",
+            "value": value, "unit": "Msamples·scales/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (device splitmix64 noise, seed 1234), broadcast from rank 0",
+            "config": {"workload": "scalogram", "desc": f"Morlet direct scalogram, {ns} scales sigma 16..16384, "
+                       f"N={n}, xi=10, P_D=6, n0=min(5, sigma/4), fp32", "shard": args.shard,
+                       "parallelism": f"{args.shard}-sharded x{world}", "n": n, "scales": ns,
+                       "l2": "step working set (>= 1 GiB of outputs) larger than L2"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": ncu_traffic("scalogram"), "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": step_bytes / max(1, launches_per_step),
+                         "kernel": "sft_scan_kernel (K1), one launch per scale", "kernel_ms": kernel_ms},
+            "e2e": {"value": e2e_value, "unit": "Msamples·scales/s", "h2d_bytes_per_step": n * 4,
+                    "d2h_bytes_per_step": sc.output_bytes(), "steps": 1,
+                    "path": "Scalogram.run (public API) with pinned host input/output"},
+            "gpu_launches": args.steps * launches_per_step,
+            "gather_ms": gather_ms,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="morlet_direct")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["scalogram"], default="morlet_direct")
+    ap.add_argument("--scalogram-n", type=int, default=1 << 24)
+    ap.add_argument("--scalogram-scales", type=int, default=128)
+    ap.add_argument("--shard", choices=["scale", "chunk"], default="scale")
+    ap.add_argument("--gather", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.workload == "scalogram":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "scalogram CPU reference is hours of CPU time; "
+                              "reference arm runs the headline workload"}))
+            return
+        return run_scalogram(args)
     w = WORKLOADS[args.workload]
 
     def spec_of():

@@ -204,6 +204,15 @@ int sftgpu_gauss_kernel_rmse(const sftgpu_gauss_bundle* b, int gauss_kind, int n
 int sftgpu_tune_beta_gauss(double sigma, int half_width, int max_order, int n0,
                            double* beta, double* rmse);
 
+/* Coefficient files, "sft-coefficients v1" text format
+ * (replaces write_coefficient_sets / read_coefficient_sets, src/coeff_io.cpp:21-101). */
+int sftgpu_write_coefficient_sets(const char* path, const sftgpu_coeffs* sets, int n_sets);
+int sftgpu_read_coefficient_sets(const char* path, sftgpu_coeffs* sets, int capacity, int* n_sets);
+/* MorletDirect spec from a stored coefficient set (the CLI's --coeffs substitution,
+ * src/cli.cpp:224-280); kernel RMSE recomputed when recompute_rmse != 0. */
+int sftgpu_make_morlet_direct_spec_from_coeffs(const sftgpu_coeffs* set, int precision, int strategy,
+                                               int recompute_rmse, sftgpu_spec* out);
+
 /* ---------------- device execution (the hot path) */
 /* Transform plan for `batch` signals of `n` samples each, laid out
  * [batch][ld_x] in device memory of the spec's precision (float/double).
@@ -212,6 +221,16 @@ int sftgpu_tune_beta_gauss(double sigma, int half_width, int max_order, int n0,
  * stream at a time (like a cuFFT plan). */
 int sftgpu_transform_plan_create(const sftgpu_spec* spec, int64_t n, int64_t batch,
                                  int boundary, sftgpu_plan** plan);
+/* Output range [out_begin, out_begin + out_count) of signals of n samples: the plan
+ * reads the samples it needs (window halo K + n0 on each side, boundary policy at the
+ * signal ends) from the full signal and writes out_count outputs. Used to shard one
+ * long signal by chunk across GPUs without any cross-GPU carry. */
+int sftgpu_transform_plan_create_range(const sftgpu_spec* spec, int64_t n, int64_t batch, int boundary,
+                                       int64_t out_begin, int64_t out_count, sftgpu_plan** plan);
+/* As _range, with an execution-mode hint: 0 auto, 1 sequential (one CTA per
+ * (signal, chunk), chunks start from their own warm-up), 2 decoupled look-back. */
+int sftgpu_transform_plan_create_ex(const sftgpu_spec* spec, int64_t n, int64_t batch, int boundary,
+                                    int64_t out_begin, int64_t out_count, int mode_hint, sftgpu_plan** plan);
 int sftgpu_transform_execute(sftgpu_plan* plan, const void* x, int64_t ld_x, void* out,
                              int64_t ld_out, void* stream);
 /* Same, from/to HOST memory of the plan's precision (host<->device copies included;
@@ -220,6 +239,9 @@ int sftgpu_transform_execute_host(sftgpu_plan* plan, const void* x_host, void* o
                                   void* stream);
 /* 1 if the transform output is complex, 0 if real. */
 int sftgpu_plan_output_is_complex(const sftgpu_plan* plan);
+/* Plan geometry: info[0..7] = {sequential, direct-convolution, positions per thread,
+ * positions per tile, warm-up tiles, chunks per signal, CTAs per launch, launches}. */
+int sftgpu_plan_describe(const sftgpu_plan* plan, int64_t* info, int n_info);
 /* Number of kernel launches one execute issues. */
 int sftgpu_plan_launches_per_execute(const sftgpu_plan* plan);
 

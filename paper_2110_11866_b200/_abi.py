@@ -121,7 +121,13 @@ SIGNATURES = {
     "sftgpu_morlet_multiply_kernel_rmse": ([_D, _D, _I, _I, _I, C.POINTER(C.c_double)], _I),
     "sftgpu_gauss_kernel_rmse": ([C.POINTER(GaussBundle), _I, _I, C.POINTER(C.c_double)], _I),
     "sftgpu_tune_beta_gauss": ([_D, _I, _I, _I, C.POINTER(C.c_double), C.POINTER(C.c_double)], _I),
+    "sftgpu_write_coefficient_sets": ([C.c_char_p, C.POINTER(Coeffs), _I], _I),
+    "sftgpu_read_coefficient_sets": ([C.c_char_p, C.POINTER(Coeffs), _I, C.POINTER(C.c_int)], _I),
+    "sftgpu_make_morlet_direct_spec_from_coeffs": ([C.POINTER(Coeffs), _I, _I, _I, C.POINTER(Spec)], _I),
     "sftgpu_transform_plan_create": ([C.POINTER(Spec), _I64, _I64, _I, C.POINTER(_P)], _I),
+    "sftgpu_transform_plan_create_range": ([C.POINTER(Spec), _I64, _I64, _I, _I64, _I64, C.POINTER(_P)], _I),
+    "sftgpu_transform_plan_create_ex": ([C.POINTER(Spec), _I64, _I64, _I, _I64, _I64, _I, C.POINTER(_P)], _I),
+    "sftgpu_plan_describe": ([_P, C.POINTER(C.c_int64), _I], _I),
     "sftgpu_transform_execute": ([_P, _P, _I64, _P, _I64, _P], _I),
     "sftgpu_transform_execute_host": ([_P, _P, _P, _P], _I),
     "sftgpu_plan_output_is_complex": ([_P], _I),

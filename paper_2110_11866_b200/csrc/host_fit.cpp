@@ -6,7 +6,10 @@
 #include <cctype>
 #include <cmath>
 #include <functional>
+#include <cstdio>
+#include <map>
 #include <numeric>
+#include <sstream>
 
 namespace sftb {
 
@@ -514,10 +517,20 @@ double morlet_multiply_kernel_rmse(const MorletP& p, int pm, int n0, Coeffs* out
 int select_optimal_ps(const MorletP& p, int pd, int n0) {
   if (pd < 1) throw std::invalid_argument("select_optimal_ps: P_D must be >= 1");
   const int hi = static_cast<int>(std::ceil(p.K * p.xi / (M_PI * p.sigma))) + pd;
+  // The true kernel on [-5K, 5K] is the same for every candidate: evaluate it once.
+  const int half = 5 * p.K;
+  std::vector<cd> truth(2 * static_cast<size_t>(half) + 1);
+  for (int n = -half; n <= half; ++n) truth[n + half] = morlet(p, n);
   int best_ps = 0;
   double best = -1.0;
   for (int ps = 0; ps <= hi; ++ps) {
-    const double r = morlet_direct_kernel_rmse(p, ps, pd, n0);
+    const Coeffs c = fit_morlet_direct(p, ps, pd, M_PI / p.K, n0);
+    const Taps t = morlet_direct_effective_taps(c, p, n0);
+    std::vector<cd> approx(truth.size(), cd(0, 0));
+    const int64_t thi = t.lo + static_cast<int64_t>(t.taps.size()) - 1;
+    for (int n = -half; n <= half; ++n)
+      if (n >= t.lo && n <= thi) approx[n + half] = t.taps[n - t.lo];
+    const double r = relative_rmse(approx, truth);
     if (best < 0.0 || r < best - 1e-12) {
       best = r;
       best_ps = ps;
@@ -751,6 +764,130 @@ Taps effective_kernel(const Spec& s) {
     case TKind::TruncMorlet: return sample_morlet(s.mparams);
   }
   throw std::invalid_argument("effective_kernel: unknown kind");
+}
+
+// ------------------------------------------------------------------ coefficient files
+// "sft-coefficients v1" text format (proj/src/coeff_io.cpp:11-101): one "set" header
+// line with key=value fields, "coeff cos|sin p re im" lines, "end".
+namespace {
+const char* kind_name(int k) {
+  switch (k) {
+    case kGaussCos: return "GaussCos";
+    case kGaussDerivSin: return "GaussDerivSin";
+    case kGaussDeriv2Cos: return "GaussDeriv2Cos";
+    case kMorletDirect: return "MorletDirect";
+    case kMorletMultiply: return "MorletMultiply";
+  }
+  return "?";
+}
+int kind_from_name(const std::string& n) {
+  for (int k = kGaussCos; k <= kMorletMultiply; ++k)
+    if (n == kind_name(k)) return k;
+  throw std::invalid_argument("unknown coefficient kind: " + n);
+}
+std::string g17(double v) {
+  char buf[40];
+  std::snprintf(buf, sizeof(buf), "%.17g", v);
+  return buf;
+}
+}  // namespace
+
+std::string write_coefficient_sets(const std::vector<Coeffs>& sets) {
+  std::string o = "sft-coefficients v1\n";
+  for (const Coeffs& c : sets) {
+    o += "set kind=" + std::string(kind_name(c.kind)) + " K=" + std::to_string(c.grid.K) + " beta=" + g17(c.grid.beta) +
+         " sigma=" + g17(c.sigma) + " xi=" + g17(c.xi) + " n0=" + std::to_string(c.n0) + " fit_rmse=" + g17(c.fit_rmse) +
+         "\n";
+    for (size_t i = 0; i < c.grid.cos_p.size(); ++i)
+      o += "coeff cos " + std::to_string(c.grid.cos_p[i]) + " " + g17(c.cc[i].real()) + " " + g17(c.cc[i].imag()) + "\n";
+    for (size_t i = 0; i < c.grid.sin_p.size(); ++i)
+      o += "coeff sin " + std::to_string(c.grid.sin_p[i]) + " " + g17(c.sc[i].real()) + " " + g17(c.sc[i].imag()) + "\n";
+    o += "end\n";
+  }
+  return o;
+}
+
+std::vector<Coeffs> read_coefficient_sets(const std::string& text) {
+  std::istringstream is(text);
+  std::string line;
+  if (!std::getline(is, line) || line != "sft-coefficients v1")
+    throw std::invalid_argument("coefficient file: bad or missing version header");
+  std::vector<Coeffs> sets;
+  while (std::getline(is, line)) {
+    if (line.empty()) continue;
+    std::istringstream head(line);
+    std::string tok;
+    head >> tok;
+    if (tok != "set") throw std::invalid_argument("coefficient file: expected 'set', got: " + line);
+    std::map<std::string, std::string> f;
+    while (head >> tok) {
+      const auto eq = tok.find('=');
+      if (eq == std::string::npos) throw std::invalid_argument("coefficient file: malformed field: " + tok);
+      f[tok.substr(0, eq)] = tok.substr(eq + 1);
+    }
+    auto need = [&](const char* k) -> const std::string& {
+      auto it = f.find(k);
+      if (it == f.end()) throw std::invalid_argument(std::string("coefficient file: missing field ") + k);
+      return it->second;
+    };
+    Coeffs c;
+    c.kind = kind_from_name(need("kind"));
+    const int K = std::stoi(need("K"));
+    const double beta = std::stod(need("beta"));
+    std::vector<int> co, so;
+    while (std::getline(is, line) && line != "end") {
+      std::istringstream row(line);
+      std::string tag, basis;
+      int p = 0;
+      double re = 0.0, im = 0.0;
+      row >> tag >> basis >> p >> re >> im;
+      if (tag != "coeff" || row.fail())
+        throw std::invalid_argument("coefficient file: malformed coefficient line: " + line);
+      if (basis == "cos") {
+        co.push_back(p);
+        c.cc.emplace_back(re, im);
+      } else if (basis == "sin") {
+        so.push_back(p);
+        c.sc.emplace_back(re, im);
+      } else {
+        throw std::invalid_argument("coefficient file: unknown basis: " + basis);
+      }
+    }
+    c.grid = Grid(K, beta, co, so);
+    c.fit_rmse = std::stod(need("fit_rmse"));
+    c.sigma = std::stod(need("sigma"));
+    c.xi = std::stod(need("xi"));
+    c.n0 = std::stoi(need("n0"));
+    sets.push_back(std::move(c));
+  }
+  return sets;
+}
+
+// A MorletDirect spec from a stored coefficient set (the CLI's --coeffs path,
+// proj/src/cli.cpp:224-280): parameters from the set's provenance, kernel RMSE
+// recomputed on [-5K, 5K] when requested.
+Spec morlet_direct_spec_from_coeffs(const Coeffs& c, int precision, int strategy, bool recompute_rmse) {
+  if (c.kind != kMorletDirect) throw std::invalid_argument("coefficient set is not MorletDirect");
+  if (c.grid.cos_p.empty()) throw std::invalid_argument("coefficient set has no cosine orders");
+  check_shift(c.sigma, c.n0);
+  Spec s;
+  s.kind = TKind::MorletDirect;
+  s.has_morlet = true;
+  s.mparams = MorletP(c.sigma, c.xi, c.grid.K);
+  s.ps = c.grid.cos_p.front();
+  s.pd = static_cast<int>(c.grid.cos_p.size());
+  s.n0 = c.n0;
+  s.alpha = shift_alpha(c.sigma, c.n0);
+  s.strategy = strategy;
+  s.precision = precision;
+  s.beta = c.grid.beta;
+  s.morlet = c;
+  s.has_mcoef = true;
+  if (recompute_rmse)
+    s.kernel_rmse = rmse_against(morlet_direct_effective_taps(c, s.mparams, c.n0), 5 * c.grid.K,
+                                 [&](double n) { return morlet(s.mparams, n); });
+  s.abbrev = encode_abbreviation(s.kind, c.n0, s.pd);
+  return s;
 }
 
 }  // namespace sftb

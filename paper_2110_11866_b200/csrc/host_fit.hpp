@@ -142,5 +142,8 @@ Taps effective_kernel(const Spec& s);
 Taps sample_gauss(const GaussP& p);
 Taps sample_morlet(const MorletP& p);
 double relative_rmse(const std::vector<cd>& approx, const std::vector<cd>& truth);
+std::string write_coefficient_sets(const std::vector<Coeffs>& sets);
+std::vector<Coeffs> read_coefficient_sets(const std::string& text);
+Spec morlet_direct_spec_from_coeffs(const Coeffs& c, int precision, int strategy, bool recompute_rmse);
 
 }  // namespace sftb

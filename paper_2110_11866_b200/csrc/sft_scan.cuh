@@ -96,9 +96,11 @@ struct ScanParams {
   int accumulate;
   int vec_ok;  // output base and row stride allow 16-byte vector stores
   int na;  // group mode 1: orders [0, na) use injection A, [na, NORD) injection B
-  long long tiles_per_signal;
+  long long tiles_per_signal;  // LB: per signal; SEQ: per chunk (warm tiles included)
   long long warm_tiles;
   long long total_tiles;  // LB: tiles in the grid
+  long long chunk_len;    // SEQ: outputs per chunk (multiple of the tile), one CTA per chunk
+  long long n_chunks;     // SEQ: chunks per signal
   // ctrl[0] ticket, ctrl[1] finished-CTA count, ctrl[2] launch epoch. The last CTA
   // of a launch resets ticket/count and bumps the epoch, so launches need no host
   // state (graph-capturable) and stale look-back flags are ignored.
@@ -292,12 +294,12 @@ __device__ __forceinline__ void lookback(const ScanParams<T>& P, Smem<T, NORD, L
 // index o0 (coalesced, element e = tid + k*NT) into registers (prefetch). Interior
 // tiles (both windows inside the signal and past the warm start) skip all checks.
 template <typename T, int L, int NT>
-__device__ __forceinline__ void fetch_tile(const ScanParams<T>& P, const T* __restrict__ xs, long long o0,
-                                           int tid, T (&fl)[L], T (&ft)[L]) {
+__device__ __forceinline__ void fetch_tile(const ScanParams<T>& P, const T* __restrict__ xs, long long lo,
+                                           long long o0, int tid, T (&fl)[L], T (&ft)[L]) {
   constexpr int TT = NT * L;
-  const long long lead_min = P.lo - P.K;  // virtual zero before the warm start
+  const long long lead_min = lo - P.K;  // virtual zero before the warm start
   const unsigned long long pol = l2_keep_policy();
-  const long long l0 = P.lo + o0 + P.K, t0 = P.lo + o0 - P.K;
+  const long long l0 = lo + o0 + P.K, t0 = lo + o0 - P.K;
   if (o0 >= 0 && t0 >= 0 && l0 + TT <= P.n && l0 >= lead_min) {
     const T* pl = xs + l0 + tid;
     const T* pt = xs + t0 + tid;
@@ -311,7 +313,7 @@ __device__ __forceinline__ void fetch_tile(const ScanParams<T>& P, const T* __re
 #pragma unroll
   for (int k = 0; k < L; ++k) {
     const long long o = o0 + tid + k * NT;
-    const long long pos = P.lo + o;
+    const long long pos = lo + o;
     const long long jl = pos + P.K;
     fl[k] = (jl >= lead_min) ? load_ext_keep(xs, P.n, P.boundary, jl, pol) : T(0);
     ft[k] = (o >= 0) ? load_ext(xs, P.n, P.boundary, pos - P.K) : T(0);
@@ -396,7 +398,8 @@ struct Cx<double> {
 // tile's on exit when `has_next`.
 template <typename T, int NORD, int NA, int GM, int MODE, int L, int NT, bool SEQ>
 __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L, NT>& S, long long sig,
-                                        long long gt, long long first, long long o0, T (&fl)[L], T (&ft)[L],
+                                        long long gt, long long first, long long lo, long long count,
+                                        long long obase, long long o0, T (&fl)[L], T (&ft)[L],
                                         const T* __restrict__ xs, bool has_next) {
   using X = Cx<T>;
   using St = typename X::S;
@@ -418,7 +421,7 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
     stl[e + (e >> 5)] = ft[k];
   }
   __syncthreads();
-  if (has_next) fetch_tile<T, L, NT>(P, xs, o0 + TT, tid, fl, ft);  // in flight during this tile
+  if (has_next) fetch_tile<T, L, NT>(P, xs, lo, o0 + TT, tid, fl, ft);  // in flight during this tile
 
   // ---- injections, shared across orders where the group mode allows
   T xt_[L];
@@ -550,13 +553,13 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
     for (int p = 0; p < NORD; ++p) {
       const OrdConst<T>& c = P.oc[p];
       St v = st[p];
-      T* cptr = P.out + p * P.ord_stride + sig * P.ld_out;
-      T* sptr = P.out_s + p * P.ord_stride + sig * P.ld_out;
+      T* cptr = P.out + p * P.ord_stride + sig * P.ld_out + obase;
+      T* sptr = P.out_s + p * P.ord_stride + sig * P.ld_out + obase;
 #pragma unroll
       for (int i = 0; i < L; ++i) {
         v = X::step(c, v, inj(c, p, i, true));
         const long long o = ob + i;
-        if (o < P.count) {
+        if (o < count) {
           // c = Re(a V + b x_t), s = -Im(a V + b x_t), a = (k1, k2), b = (k3, k4) = (ka[1], kb[1])
           const T vr = X::re(v), vi = X::im(v), xt = xt_[i];
           cptr[o] = fma(c.ka[0], vr, fma(-c.kb[0], vi, c.ka[1] * xt));
@@ -600,9 +603,9 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
         buf[i] = accr[i];
       }
     }
-    T* optr = P.out + CW * (sig * P.ld_out);
+    T* optr = P.out + CW * (sig * P.ld_out + obase);
     constexpr int VW = 16 / sizeof(T);  // T words per 16-byte vector
-    if (P.vec_ok && !P.accumulate && ob + L <= P.count && (L * CW) % VW == 0) {
+    if (P.vec_ok && !P.accumulate && ob + L <= count && (L * CW) % VW == 0) {
       T* dst = optr + ob * CW;
 #pragma unroll
       for (int v = 0; v < L * CW / VW; ++v) {
@@ -616,7 +619,7 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
 #pragma unroll
       for (int i = 0; i < L; ++i) {
         const long long o = ob + i;
-        if (o < P.count) {
+        if (o < count) {
 #pragma unroll
           for (int w = 0; w < CW; ++w) {
             if (P.accumulate)
@@ -640,15 +643,21 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? 4 : 2)) sft_scan_kernel(
   T fl[L], ft[L];
 
   if constexpr (SEQ) {
-    // one CTA per signal, tiles in order, carry in shared memory
-    const long long sig = blockIdx.x;
+    // one CTA per (signal, chunk): tiles in order from the chunk's own warm start,
+    // carry in shared memory
+    const long long sig = blockIdx.x / P.n_chunks;
+    const long long ch = blockIdx.x - sig * P.n_chunks;
+    const long long obase = ch * P.chunk_len;
+    const long long lo = P.lo + obase;
+    const long long count = P.count - obase < P.chunk_len ? P.count - obase : P.chunk_len;
+    const long long tiles = P.warm_tiles + (count + TT - 1) / TT;
     const T* __restrict__ xs = P.x + sig * P.ld_x;
     if (tid < NORD) S.carry[tid] = make_double2(0.0, 0.0);
     const long long o_first = -P.warm_tiles * TT;
-    fetch_tile<T, L, NT>(P, xs, o_first, tid, fl, ft);
-    for (long long t = 0; t < P.tiles_per_signal; ++t)
-      do_tile<T, NORD, NA, GM, MODE, L, NT, true>(P, S, sig, 0, 0, o_first + t * TT, fl, ft, xs,
-                                              t + 1 < P.tiles_per_signal);
+    fetch_tile<T, L, NT>(P, xs, lo, o_first, tid, fl, ft);
+    for (long long t = 0; t < tiles; ++t)
+      do_tile<T, NORD, NA, GM, MODE, L, NT, true>(P, S, sig, 0, 0, lo, count, obase, o_first + t * TT, fl, ft, xs,
+                                                  t + 1 < tiles);
   } else {
     if (tid == 0) {
       S.tile = static_cast<long long>(atomicAdd(P.ctrl, 1u));
@@ -660,8 +669,8 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? 4 : 2)) sft_scan_kernel(
     const long long first = sig * P.tiles_per_signal;
     const long long o0 = (gt - first - P.warm_tiles) * TT;
     const T* __restrict__ xs = P.x + sig * P.ld_x;
-    fetch_tile<T, L, NT>(P, xs, o0, tid, fl, ft);
-    do_tile<T, NORD, NA, GM, MODE, L, NT, false>(P, S, sig, gt, first, o0, fl, ft, xs, false);
+    fetch_tile<T, L, NT>(P, xs, P.lo, o0, tid, fl, ft);
+    do_tile<T, NORD, NA, GM, MODE, L, NT, false>(P, S, sig, gt, first, P.lo, P.count, 0, o0, fl, ft, xs, false);
   }
 }
 

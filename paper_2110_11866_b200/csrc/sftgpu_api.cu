@@ -103,7 +103,9 @@ struct sftgpu_plan {
   long long n = 0, batch = 0, lo = 0, count = 0;
   int K = 1, boundary = SFTGPU_BOUNDARY_CLAMP;
   int L = 8, NT = 128;
-  int seq = 0;  // 1: one CTA walks a whole signal (batched), no look-back workspace
+  int seq = 0;  // 1: one CTA walks a whole (signal, chunk), no look-back workspace
+  int mode_hint = 0;  // 0 auto, 1 force SEQ (chunked), 2 force LB
+  long long n_chunks = 1, chunk_len = 0;
   long long TT = 1024, tiles_per_signal = 0, warm_tiles = 0, total_tiles = 0;
   std::vector<Group> groups;
   int max_nord = 1;
@@ -145,7 +147,7 @@ size_t elem_size(int precision) { return precision == SFTGPU_SINGLE ? sizeof(flo
 template <typename T>
 void launch_scan(const sftgpu_plan* pl, const Group& g, const sftk::ScanParams<T>& p, cudaStream_t s) {
   if (g.nord < 1 || g.nord > sftk::kMaxOrd) fail(SFTGPU_EINTERNAL, "order group size out of range");
-  const long long grid = pl->seq ? pl->batch : pl->total_tiles;
+  const long long grid = pl->seq ? pl->batch * pl->n_chunks : pl->total_tiles;
   const sftk::LaunchKey key{g.nord, g.gm, pl->mode, pl->seq};
   switch (pl->mode) {
     case sftk::kModeReal:
@@ -345,17 +347,44 @@ void build_groups(sftgpu_plan* pl, std::vector<Order> ords, double alpha, double
   for (const Group& g : pl->groups) pl->max_nord = std::max(pl->max_nord, g.nord);
 }
 
-// SEQ (one CTA per signal) when the batch alone fills the GPU; LB (one tile per CTA
-// with look-back) otherwise. Tile geometry per mode/precision (sftk::Geometry).
+// Geometry. SEQ: one CTA per (signal, chunk); a chunk starts from its own warm-up
+// 2K positions early (phase-1 work only), so chunks are kept >= 8 tiles and >= 16K
+// positions long (warm-up <= ~1/8 of the chunk's positions). LB: one tile per CTA
+// with look-back. Auto picks SEQ when the (signal, chunk) grid gives >= 2 CTAs per SM.
 void choose_geometry(sftgpu_plan* pl) {
-  pl->seq = (!pl->is_components && pl->batch >= 256) ? 1 : 0;
   const bool dbl = pl->precision == SFTGPU_DOUBLE;
+  constexpr long long kSms = 148, kTarget = 4 * kSms;
   pl->NT = sftk::kThreads;
-  pl->L = pl->seq ? (dbl ? sftk::kLSeqF64 : sftk::kLSeqF32) : (dbl ? sftk::kLLbF64 : sftk::kLLbF32);
+  const long long tt_seq = static_cast<long long>(dbl ? sftk::kLSeqF64 : sftk::kLSeqF32) * pl->NT;
+  const long long cmin = ((std::max(8 * tt_seq, 16LL * pl->K) + tt_seq - 1) / tt_seq) * tt_seq;
+  const long long max_chunks = std::max(1LL, (pl->count + cmin - 1) / cmin);
+  const long long want = std::max(1LL, (kTarget + pl->batch - 1) / pl->batch);
+  long long chunks = std::min(max_chunks, want);
+  bool seq;
+  if (pl->is_components)
+    seq = false;
+  else if (pl->mode_hint == 1)
+    seq = true;
+  else if (pl->mode_hint == 2)
+    seq = false;
+  else
+    seq = pl->batch * chunks >= 2 * kSms;
+  pl->seq = seq ? 1 : 0;
+  pl->L = seq ? (dbl ? sftk::kLSeqF64 : sftk::kLSeqF32) : (dbl ? sftk::kLLbF64 : sftk::kLLbF32);
   pl->TT = static_cast<long long>(pl->L) * pl->NT;
   pl->warm_tiles = (2LL * pl->K + pl->TT - 1) / pl->TT;
-  pl->tiles_per_signal = pl->warm_tiles + (pl->count + pl->TT - 1) / pl->TT;
-  pl->total_tiles = pl->tiles_per_signal * pl->batch;
+  if (seq) {
+    const long long per = (pl->count + chunks - 1) / chunks;
+    pl->chunk_len = ((per + pl->TT - 1) / pl->TT) * pl->TT;
+    pl->n_chunks = (pl->count + pl->chunk_len - 1) / pl->chunk_len;
+    pl->tiles_per_signal = pl->warm_tiles + pl->chunk_len / pl->TT;
+    pl->total_tiles = pl->batch * pl->n_chunks;
+  } else {
+    pl->n_chunks = 1;
+    pl->chunk_len = pl->count;
+    pl->tiles_per_signal = pl->warm_tiles + (pl->count + pl->TT - 1) / pl->TT;
+    pl->total_tiles = pl->tiles_per_signal * pl->batch;
+  }
 }
 
 void alloc_workspace(sftgpu_plan* pl) {
@@ -625,6 +654,8 @@ void run_groups(sftgpu_plan* pl, const void* x, long long ld_x, void* out, void*
     P.tiles_per_signal = pl->tiles_per_signal;
     P.warm_tiles = pl->warm_tiles;
     P.total_tiles = pl->total_tiles;
+    P.chunk_len = pl->chunk_len;
+    P.n_chunks = pl->n_chunks;
     P.ctrl = pl->d_ctrl;
     P.flags = pl->d_flags;
     P.agg = pl->d_agg;
@@ -779,15 +810,69 @@ int sftgpu_tune_beta_gauss(double sigma, int K, int P, int n0, double* beta, dou
   });
 }
 
+int sftgpu_write_coefficient_sets(const char* path, const sftgpu_coeffs* sets, int n_sets) {
+  return guarded([&] {
+    if (!path || (!sets && n_sets > 0)) fail(SFTGPU_EINVAL, "null argument");
+    std::vector<sftb::Coeffs> v;
+    for (int i = 0; i < n_sets; ++i) v.push_back(coeffs_from_c(&sets[i]));
+    const std::string text = sftb::write_coefficient_sets(v);
+    FILE* f = std::fopen(path, "wb");
+    if (!f) fail(SFTGPU_EINVAL, std::string("cannot open coefficient file: ") + path);
+    const size_t w = std::fwrite(text.data(), 1, text.size(), f);
+    std::fclose(f);
+    if (w != text.size()) fail(SFTGPU_EINTERNAL, "short write to coefficient file");
+  });
+}
+
+int sftgpu_read_coefficient_sets(const char* path, sftgpu_coeffs* sets, int capacity, int* n_sets) {
+  return guarded([&] {
+    if (!path || !n_sets) fail(SFTGPU_EINVAL, "null argument");
+    FILE* f = std::fopen(path, "rb");
+    if (!f) fail(SFTGPU_EINVAL, std::string("cannot open coefficient file: ") + path);
+    std::string text;
+    char buf[65536];
+    size_t r;
+    while ((r = std::fread(buf, 1, sizeof(buf), f)) > 0) text.append(buf, r);
+    std::fclose(f);
+    const std::vector<sftb::Coeffs> v = sftb::read_coefficient_sets(text);
+    *n_sets = static_cast<int>(v.size());
+    if (sets) {
+      if (capacity < *n_sets) fail(SFTGPU_EINVAL, "coefficient set buffer too small");
+      for (size_t i = 0; i < v.size(); ++i) coeffs_to_c(v[i], &sets[i]);
+    }
+  });
+}
+
+int sftgpu_make_morlet_direct_spec_from_coeffs(const sftgpu_coeffs* set, int precision, int strategy,
+                                               int recompute_rmse, sftgpu_spec* out) {
+  return guarded([&] {
+    if (!set || !out) fail(SFTGPU_EINVAL, "null argument");
+    spec_to_c(sftb::morlet_direct_spec_from_coeffs(coeffs_from_c(set), precision, strategy, recompute_rmse != 0),
+              out);
+  });
+}
+
 int sftgpu_transform_plan_create(const sftgpu_spec* spec, int64_t n, int64_t batch, int boundary,
                                  sftgpu_plan** plan) {
+  return sftgpu_transform_plan_create_range(spec, n, batch, boundary, 0, n, plan);
+}
+
+int sftgpu_transform_plan_create_range(const sftgpu_spec* spec, int64_t n, int64_t batch, int boundary,
+                                       int64_t out_begin, int64_t out_count, sftgpu_plan** plan) {
+  return sftgpu_transform_plan_create_ex(spec, n, batch, boundary, out_begin, out_count, 0, plan);
+}
+
+int sftgpu_transform_plan_create_ex(const sftgpu_spec* spec, int64_t n, int64_t batch, int boundary,
+                                    int64_t out_begin, int64_t out_count, int mode_hint, sftgpu_plan** plan) {
   return guarded([&] {
+    if (mode_hint < 0 || mode_hint > 2) fail(SFTGPU_EINVAL, "mode_hint must be 0 (auto), 1 (sequential), 2 (look-back)");
     if (!plan) fail(SFTGPU_EINVAL, "null plan pointer");
     *plan = nullptr;
     if (n < 1) fail(SFTGPU_EINVAL, "Signal: need at least one sample");
     if (batch < 1) fail(SFTGPU_EINVAL, "batch must be >= 1");
     if (boundary != SFTGPU_BOUNDARY_ZERO && boundary != SFTGPU_BOUNDARY_CLAMP)
       fail(SFTGPU_EINVAL, "unknown boundary policy");
+    if (out_begin < 0 || out_count < 1 || out_begin + out_count > n) fail(SFTGPU_EINVAL, "output range outside the signal");
     const sftb::Spec s = spec_from_c(spec);
     require_device();
     auto pl = std::make_unique<sftgpu_plan>();
@@ -797,6 +882,7 @@ int sftgpu_transform_plan_create(const sftgpu_spec* spec, int64_t n, int64_t bat
     pl->batch = batch;
     pl->boundary = boundary;
     if (s.kind == sftb::TKind::TruncGauss || s.kind == sftb::TKind::TruncMorlet) {
+      if (out_begin != 0 || out_count != n) fail(SFTGPU_EINVAL, "truncated-convolution plans cover the whole signal");
       const sftb::Taps t = sftb::effective_kernel(s);
       pl->conv = 1;
       pl->mode = s.kind == sftb::TKind::TruncMorlet ? sftk::kModeComplex : sftk::kModeReal;
@@ -814,9 +900,10 @@ int sftgpu_transform_plan_create(const sftgpu_spec* spec, int64_t n, int64_t bat
     }
     const Lowered lw = lower_spec(s);
     pl->K = lw.K;
-    pl->lo = -static_cast<long long>(s.n0);  // window read at n - n0 (transforms.cpp:287-288)
-    pl->count = n;
+    pl->lo = out_begin - static_cast<long long>(s.n0);  // window read at n - n0 (transforms.cpp:287-288)
+    pl->count = out_count;
     pl->mode = lw.complex_out ? sftk::kModeComplex : sftk::kModeReal;
+    pl->mode_hint = mode_hint;
     choose_geometry(pl.get());
     if (pl->precision == SFTGPU_SINGLE)
       build_groups<float>(pl.get(), lw.orders, lw.alpha, lw.prefactor, false);
@@ -883,7 +970,7 @@ int sftgpu_transform_execute(sftgpu_plan* pl, const void* x, int64_t ld_x, void*
   return guarded([&] {
     if (!pl || pl->is_components) fail(SFTGPU_EINVAL, "not a transform plan");
     if (!x || !out) fail(SFTGPU_EINVAL, "null buffer");
-    if (ld_x < pl->n || ld_out < pl->n) fail(SFTGPU_EINVAL, "leading dimension smaller than n");
+    if (ld_x < pl->n || ld_out < pl->count) fail(SFTGPU_EINVAL, "leading dimension smaller than the row length");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (pl->conv) {
       run_conv(pl, x, ld_x, out, ld_out, st);
@@ -902,7 +989,7 @@ int sftgpu_transform_execute_host(sftgpu_plan* pl, const void* x_host, void* out
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t es = elem_size(pl->precision);
     const size_t xb = static_cast<size_t>(pl->n * pl->batch) * es;
-    const size_t ob = xb * (pl->mode == sftk::kModeComplex ? 2 : 1);
+    const size_t ob = static_cast<size_t>(pl->count * pl->batch) * es * (pl->mode == sftk::kModeComplex ? 2 : 1);
     if (pl->cap_x < xb) {
       cudaFree(pl->d_x);
       pl->d_x = nullptr;
@@ -919,9 +1006,9 @@ int sftgpu_transform_execute_host(sftgpu_plan* pl, const void* x_host, void* out
     if (pl->conv) {
       run_conv(pl, pl->d_x, pl->n, pl->d_out, pl->n, st);
     } else if (pl->precision == SFTGPU_SINGLE) {
-      run_groups<float>(pl, pl->d_x, pl->n, pl->d_out, nullptr, pl->n, 0, st);
+      run_groups<float>(pl, pl->d_x, pl->n, pl->d_out, nullptr, pl->count, 0, st);
     } else {
-      run_groups<double>(pl, pl->d_x, pl->n, pl->d_out, nullptr, pl->n, 0, st);
+      run_groups<double>(pl, pl->d_x, pl->n, pl->d_out, nullptr, pl->count, 0, st);
     }
     cuda_check(cudaMemcpyAsync(out_host, pl->d_out, ob, cudaMemcpyDeviceToHost, st), "D2H");
     cuda_check(cudaStreamSynchronize(st), "stream sync");
@@ -929,6 +1016,15 @@ int sftgpu_transform_execute_host(sftgpu_plan* pl, const void* x_host, void* out
 }
 
 int sftgpu_plan_output_is_complex(const sftgpu_plan* pl) { return pl && pl->mode == sftk::kModeComplex ? 1 : 0; }
+
+int sftgpu_plan_describe(const sftgpu_plan* pl, int64_t* info, int n_info) {
+  return guarded([&] {
+    if (!pl || !info) fail(SFTGPU_EINVAL, "null argument");
+    const int64_t v[8] = {pl->seq, pl->conv, pl->L * 1LL, pl->TT, pl->warm_tiles, pl->n_chunks, pl->total_tiles,
+                          static_cast<int64_t>(pl->groups.size())};
+    for (int i = 0; i < n_info && i < 8; ++i) info[i] = v[i];
+  });
+}
 
 int sftgpu_plan_launches_per_execute(const sftgpu_plan* pl) {
   if (!pl) return 0;

@@ -29,7 +29,8 @@ __all__ = [
     "truncated_convolution", "fit_gaussian_bundle", "fit_morlet_direct", "fit_morlet_envelope",
     "fit_mmse", "select_optimal_ps", "tune_beta_gauss", "gauss_kernel_rmse",
     "morlet_direct_kernel_rmse", "morlet_multiply_kernel_rmse", "TransformPlan", "ComponentsPlan",
-    "FitDegenerateError", "SftGpuError",
+    "FitDegenerateError", "SftGpuError", "write_coefficient_sets", "read_coefficient_sets",
+    "morlet_direct_spec_from_coeffs",
 ]
 
 
@@ -394,6 +395,38 @@ def make_morlet_multiply_spec(sigma, xi, pm: int, n0: int, options=None) -> Tran
     return TransformSpec(raw)
 
 
+def write_coefficient_sets(path: str, sets) -> None:
+    """"sft-coefficients v1" file (proj/src/coeff_io.cpp:21-42); ``sets`` are
+    TransformSpec (their fitted set) or raw ``_abi.Coeffs``."""
+    raws = []
+    for s_ in sets:
+        if isinstance(s_, TransformSpec):
+            k = s_.kind
+            raws.append(s_._raw.morlet if k == TransformKind.MorletDirect else s_._raw.envelope)
+        else:
+            raws.append(s_)
+    arr = (_abi.Coeffs * max(1, len(raws)))(*raws)
+    check(lib().sftgpu_write_coefficient_sets(path.encode(), arr, len(raws)))
+
+
+def read_coefficient_sets(path: str):
+    """Raw coefficient sets from an "sft-coefficients v1" file (coeff_io.cpp:44-101)."""
+    n = C.c_int()
+    check(lib().sftgpu_read_coefficient_sets(path.encode(), None, 0, C.byref(n)))
+    arr = (_abi.Coeffs * max(1, n.value))()
+    check(lib().sftgpu_read_coefficient_sets(path.encode(), arr, n.value, C.byref(n)))
+    return [arr[i] for i in range(n.value)]
+
+
+def morlet_direct_spec_from_coeffs(raw: "_abi.Coeffs", precision=Precision.Double, strategy=Strategy.Recursive2,
+                                   recompute_rmse: bool = True) -> TransformSpec:
+    """A MorletDirect spec from a stored coefficient set (proj/src/cli.cpp:224-280)."""
+    spec = _abi.Spec()
+    check(lib().sftgpu_make_morlet_direct_spec_from_coeffs(C.byref(raw), int(precision), int(strategy),
+                                                           int(recompute_rmse), C.byref(spec)))
+    return TransformSpec(spec)
+
+
 @dataclass
 class KernelTaps:  # include/sft/kernels.hpp:76-81
     taps: np.ndarray
@@ -484,17 +517,30 @@ class TransformResult:  # include/sft/transforms.hpp:74-81
 class TransformPlan:
     """Device plan: ``batch`` signals of ``n`` samples -> transform output, all in HBM.
     x: [batch][ld_x] (float32 for Single, float64 for Double); out: [batch][ld_out]
-    real, or [batch][ld_out][2] complex interleaved."""
+    real, or [batch][ld_out][2] complex interleaved. ``out_range=(begin, count)``
+    computes only outputs [begin, begin+count) (chunk sharding with halo)."""
 
-    def __init__(self, spec: TransformSpec, n: int, batch: int = 1, boundary=BoundaryPolicy.Clamp):
+    MODES = {"auto": 0, "seq": 1, "lookback": 2}
+
+    def __init__(self, spec: TransformSpec, n: int, batch: int = 1, boundary=BoundaryPolicy.Clamp,
+                 out_range=None, mode: str = "auto"):
         h = C.c_void_p()
-        check(lib().sftgpu_transform_plan_create(C.byref(spec._raw), n, batch, int(boundary), C.byref(h)))
+        begin, count = out_range if out_range is not None else (0, n)
+        check(lib().sftgpu_transform_plan_create_ex(C.byref(spec._raw), n, batch, int(boundary), begin, count,
+                                                    self.MODES[mode], C.byref(h)))
         self._h = h
-        self.n, self.batch = n, batch
+        self.n, self.batch, self.out_begin, self.count = n, batch, begin, count
         self.complex_out = bool(lib().sftgpu_plan_output_is_complex(h))
         conv = spec.kind in (TransformKind.TruncConvGauss, TransformKind.TruncConvMorlet)
         self.precision = Precision.Double if conv else spec.precision
         self.launches = lib().sftgpu_plan_launches_per_execute(h)
+
+    def describe(self) -> dict:
+        info = (C.c_int64 * 8)()
+        check(lib().sftgpu_plan_describe(self._h, info, 8))
+        keys = ("sequential", "direct_convolution", "positions_per_thread", "positions_per_tile", "warm_tiles",
+                "chunks_per_signal", "ctas_per_launch", "launches")
+        return dict(zip(keys, list(info)))
 
     def dtype(self):
         torch = _torch()
@@ -502,14 +548,14 @@ class TransformPlan:
 
     def empty_output(self):
         torch = _torch()
-        shape = (self.batch, self.n, 2) if self.complex_out else (self.batch, self.n)
+        shape = (self.batch, self.count, 2) if self.complex_out else (self.batch, self.count)
         return torch.empty(shape, dtype=self.dtype(), device="cuda")
 
     def execute(self, x, out, stream=None, ld_x=None, ld_out=None):
         torch = _torch()
         st = C.c_void_p(stream) if stream is not None else _stream_ptr(torch)
         check(lib().sftgpu_transform_execute(self._h, C.c_void_p(x.data_ptr()), ld_x or self.n,
-                                             C.c_void_p(out.data_ptr()), ld_out or self.n, st))
+                                             C.c_void_p(out.data_ptr()), ld_out or self.count, st))
 
     def execute_host(self, x_host: np.ndarray, out_host: np.ndarray, stream=None):
         torch = _torch()

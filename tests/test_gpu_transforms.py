@@ -336,3 +336,79 @@ def test_batched_seq_mode_vs_oracle(sft, O, abbrev, sigma, xi, prec, tol):
         r = o1.double().cpu().numpy()[0]
         r = r[..., 0] + 1j * r[..., 1] if plan.complex_out else r
         assert rel_max(vals[b], r) < tol
+
+
+@pytest.mark.parametrize("prec,tol", [(0, 2e-6), (1, 1e-12)])
+def test_range_plans_match_full_transform(sft, O, prec, tol):
+    """Chunk sharding: plans over an output range [b, b+c) read their halo from the full
+    signal and reproduce the full transform's rows (boundary chunks included)."""
+    import torch
+
+    spec = sft.make_transform_spec("MDS3P6", 40.0, 8.0, sft.TransformOptions(precision=prec))
+    n = 10007
+    x = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 5, 1, sft.Precision(prec))
+    full = sft.TransformPlan(spec, n)
+    fo = full.empty_output()
+    full.execute(x, fo)
+    for b, c in ((0, 1), (0, 2500), (2500, 2500), (9000, 1007), (n - 1, 1), (123, 9000)):
+        p = sft.TransformPlan(spec, n, 1, sft.BoundaryPolicy.Clamp, (b, c))
+        po = p.empty_output()
+        p.execute(x, po)
+        torch.cuda.synchronize()
+        a = po[0].double().cpu().numpy()
+        r = fo[0, b:b + c].double().cpu().numpy()
+        assert np.max(np.abs(a - r)) <= tol * np.max(np.abs(fo.double().cpu().numpy()))
+
+
+def test_scalogram_single_gpu_vs_oracle(sft, O):
+    """Config 5 shape on a reduced grid: every scale row vs the oracle, both shardings
+    (world=1) agree."""
+    import torch
+
+    from paper_2110_11866_b200 import scalogram as SG
+
+    sig = SG.scale_sigmas(6, 16.0, 256.0)
+    specs = SG.build_specs(sig, xi=10.0, pd=6)
+    n = 20000
+    x = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 1234, 1, sft.Precision.Single)[0]
+    sc = SG.Scalogram(n, specs)
+    out = sc.empty_output()
+    sc.run(x, out)
+    torch.cuda.synchronize()
+    xh = x.double().cpu().numpy()
+    o = out.double().cpu().numpy()
+    for r, i in enumerate(sc.rows):
+        s = specs[i]
+        c = s.morlet_coeffs
+        ref = O.morlet_direct(xh, 1, s.half_width, s.beta, s.n0, s.alpha, 1.0 / (2 * s.sigma ** 2), O.KERNEL_INTEGRAL,
+                              O.DOUBLE, c.cos_orders, c.cos_coeffs, c.sin_orders, c.sin_coeffs)
+        assert rel_max(o[r, :, 0] + 1j * o[r, :, 1], ref) < 1e-5
+
+
+@pytest.mark.parametrize("abbrev,sigma,xi,prec,tol", [("MDS3P6", 40.0, 8.0, 0, 2e-6), ("GDP6", 300.0, 0.0, 1, 1e-12),
+                                                      ("MMS5P3", 100.0, 10.0, 0, 2e-6)])
+def test_chunked_sequential_matches_lookback(sft, O, abbrev, sigma, xi, prec, tol):
+    """A long single signal in sequential mode is split into chunks that each start from
+    their own warm-up; it must agree with the look-back path and with the oracle."""
+    import torch
+
+    spec = sft.make_transform_spec(abbrev, sigma, xi, sft.TransformOptions(precision=prec))
+    n = 300007
+    x = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 11, 1, sft.Precision(prec))
+    outs = {}
+    for mode in ("seq", "lookback"):
+        p = sft.TransformPlan(spec, n, 1, mode=mode)
+        d = p.describe()
+        assert d["sequential"] == (mode == "seq")
+        if mode == "seq":
+            assert d["chunks_per_signal"] > 1
+        o = p.empty_output()
+        p.execute(x, o)
+        torch.cuda.synchronize()
+        outs[mode] = o[0].double().cpu().numpy()
+    scale = np.max(np.abs(outs["lookback"]))
+    assert np.max(np.abs(outs["seq"] - outs["lookback"])) <= tol * scale
+    xh = x[0].double().cpu().numpy()
+    ref = oracle_transform(O, xh, 1, spec)
+    got = outs["seq"][..., 0] + 1j * outs["seq"][..., 1] if outs["seq"].ndim == 2 else outs["seq"]
+    assert rel_max(got, ref) < (1e-5 if prec == 0 else 1e-12)
