@@ -255,6 +255,10 @@ int sftgpu_components_plan_create(const sftgpu_config* cfgs, int n_orders, int64
 int sftgpu_components_execute(sftgpu_plan* plan, const void* x, void* c, void* s,
                               void* stream);
 
+/* Same, from/to HOST memory of the plan's precision; synchronises `stream`. */
+int sftgpu_components_execute_host(sftgpu_plan* plan, const void* x_host, void* c_host, void* s_host,
+                                   void* stream);
+
 void sftgpu_plan_destroy(sftgpu_plan* plan);
 
 /* Device splitmix64 signal generator, bit-identical to make_test_signal
@@ -268,6 +272,11 @@ int sftgpu_generate_signal(int kind, int64_t n, uint64_t seed, int64_t batch, in
 int sftgpu_truncated_convolution(const double* x, int64_t n, int boundary,
                                  const double* taps, int64_t n_taps, int64_t tap_lo,
                                  double* out, void* stream);
+/* Host-memory variants (device buffers managed internally; synchronous). */
+int sftgpu_generate_signal_host(int kind, int64_t n, uint64_t seed, double* out_host);
+int sftgpu_truncated_convolution_host(const double* x_host, int64_t n, int boundary,
+                                      const double* taps_host, int64_t n_taps, int64_t tap_lo,
+                                      double* out_host);
 
 #ifdef __cplusplus
 }

@@ -134,7 +134,10 @@ SIGNATURES = {
     "sftgpu_plan_launches_per_execute": ([_P], _I),
     "sftgpu_components_plan_create": ([C.POINTER(Config), _I, _I64, _I64, _I, _I64, _I64, _I, C.POINTER(_P)], _I),
     "sftgpu_components_execute": ([_P, _P, _P, _P, _P], _I),
+    "sftgpu_components_execute_host": ([_P, _P, _P, _P, _P], _I),
     "sftgpu_plan_destroy": ([_P], None),
+    "sftgpu_generate_signal_host": ([_I, _I64, _U64, _P], _I),
+    "sftgpu_truncated_convolution_host": ([_P, _I64, _I, _P, _I64, _I64, _P], _I),
     "sftgpu_generate_signal": ([_I, _I64, _U64, _I64, _I, _P, _P], _I),
     "sftgpu_truncated_convolution": ([_P, _I64, _I, _P, _I64, _I64, _P, _P], _I),
 }

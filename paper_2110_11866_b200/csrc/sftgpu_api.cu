@@ -1044,6 +1044,40 @@ int sftgpu_components_execute(sftgpu_plan* pl, const void* x, void* c, void* s, 
   });
 }
 
+int sftgpu_components_execute_host(sftgpu_plan* pl, const void* x_host, void* c_host, void* s_host, void* stream) {
+  return guarded([&] {
+    if (!pl || !pl->is_components) fail(SFTGPU_EINVAL, "not a components plan");
+    if (!x_host || !c_host || !s_host) fail(SFTGPU_EINVAL, "null buffer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t es = elem_size(pl->precision);
+    const size_t xb = static_cast<size_t>(pl->n * pl->batch) * es;
+    size_t nord = 0;
+    for (const Group& g : pl->groups) nord += g.nord;
+    const size_t ob = nord * static_cast<size_t>(pl->batch * pl->count) * es;
+    if (pl->cap_x < xb) {
+      cudaFree(pl->d_x);
+      pl->d_x = nullptr;
+      cuda_check(cudaMalloc(&pl->d_x, xb), "cudaMalloc staging x");
+      pl->cap_x = xb;
+    }
+    if (pl->cap_out < 2 * ob) {
+      cudaFree(pl->d_out);
+      pl->d_out = nullptr;
+      cuda_check(cudaMalloc(&pl->d_out, 2 * ob), "cudaMalloc staging out");
+      pl->cap_out = 2 * ob;
+    }
+    char* dc = static_cast<char*>(pl->d_out);
+    cuda_check(cudaMemcpyAsync(pl->d_x, x_host, xb, cudaMemcpyHostToDevice, st), "H2D");
+    if (pl->precision == SFTGPU_SINGLE)
+      run_groups<float>(pl, pl->d_x, pl->n, dc, dc + ob, pl->count, 0, st);
+    else
+      run_groups<double>(pl, pl->d_x, pl->n, dc, dc + ob, pl->count, 0, st);
+    cuda_check(cudaMemcpyAsync(c_host, dc, ob, cudaMemcpyDeviceToHost, st), "D2H c");
+    cuda_check(cudaMemcpyAsync(s_host, dc + ob, ob, cudaMemcpyDeviceToHost, st), "D2H s");
+    cuda_check(cudaStreamSynchronize(st), "stream sync");
+  });
+}
+
 void sftgpu_plan_destroy(sftgpu_plan* pl) { delete pl; }
 
 int sftgpu_generate_signal(int kind, int64_t n, uint64_t seed, int64_t batch, int dtype, void* out, void* stream) {
@@ -1078,3 +1112,47 @@ int sftgpu_truncated_convolution(const double* x, int64_t n, int boundary, const
 }
 
 }  // extern "C"
+
+namespace {
+// RAII device buffer for the synchronous host-memory helpers.
+struct DevBuf {
+  void* p = nullptr;
+  explicit DevBuf(size_t bytes) { cuda_check(cudaMalloc(&p, bytes), "cudaMalloc"); }
+  ~DevBuf() { cudaFree(p); }
+};
+}  // namespace
+
+extern "C" int sftgpu_generate_signal_host(int kind, int64_t n, uint64_t seed, double* out_host) {
+  return guarded([&] {
+    if (!out_host) fail(SFTGPU_EINVAL, "null buffer");
+    if (n < 1) fail(SFTGPU_EINVAL, "make_test_signal: N must be >= 1");
+    require_device();
+    DevBuf d(static_cast<size_t>(n) * sizeof(double));
+    const int rc = sftgpu_generate_signal(kind, n, seed, 1, SFTGPU_DOUBLE, d.p, nullptr);
+    if (rc != SFTGPU_OK) fail(rc, g_err);
+    cuda_check(cudaMemcpy(out_host, d.p, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+extern "C" int sftgpu_truncated_convolution_host(const double* x_host, int64_t n, int boundary, const double* taps_host,
+                                                 int64_t n_taps, int64_t tap_lo, double* out_host) {
+  return guarded([&] {
+    if (!x_host || !taps_host || !out_host) fail(SFTGPU_EINVAL, "null buffer");
+    if (n < 1) fail(SFTGPU_EINVAL, "Signal: need at least one sample");
+    if (n_taps < 1) fail(SFTGPU_EINVAL, "truncated_convolution: empty kernel");
+    require_device();
+    DevBuf dx(static_cast<size_t>(n) * sizeof(double)), dt(static_cast<size_t>(n_taps) * 2 * sizeof(double)),
+        dout(static_cast<size_t>(n) * 2 * sizeof(double));
+    cuda_check(cudaMemcpy(dx.p, x_host, static_cast<size_t>(n) * sizeof(double), cudaMemcpyHostToDevice), "H2D x");
+    cuda_check(cudaMemcpy(dt.p, taps_host, static_cast<size_t>(n_taps) * 2 * sizeof(double), cudaMemcpyHostToDevice),
+               "H2D taps");
+    const int rc = sftgpu_truncated_convolution(static_cast<const double*>(dx.p), n, boundary,
+                                                static_cast<const double*>(dt.p), n_taps, tap_lo,
+                                                static_cast<double*>(dout.p), nullptr);
+    if (rc != SFTGPU_OK) fail(rc, g_err);
+    cuda_check(cudaMemcpy(out_host, dout.p, static_cast<size_t>(n) * 2 * sizeof(double), cudaMemcpyDeviceToHost),
+               "D2H");
+  });
+}
+
+

@@ -198,3 +198,44 @@ def test_config3_spec_matches_survey_probe(sft):
     """MDS5P6 at sigma=8192, xi=10 -> P_S = 7, kernel RMSE 0.6127%."""
     s = sft.make_transform_spec("MDS5P6", 8192.0, 10.0, sft.TransformOptions(precision=sft.Precision.Single))
     assert s.ps == 7 and s.half_width == 24576 and f"{s.kernel_rmse_percent:.4f}" == "0.6127"
+
+
+def test_coefficient_file_round_trip(sft, tmp_path):
+    """proj/tests/test_fourier_fit.cpp:210-241: sets survive the "sft-coefficients v1"
+    text format bit-for-bit (%.17g); a bad header is rejected."""
+    direct = sft.make_morlet_direct_spec(60.0, 10.0, 6, 5, sft.TransformOptions(half_width=120))
+    path = str(tmp_path / "c.coef")
+    sft.write_coefficient_sets(path, [direct])
+    text = open(path).read()
+    assert text.startswith("sft-coefficients v1\nset kind=MorletDirect K=120 ")
+    loaded = sft.read_coefficient_sets(path)
+    assert len(loaded) == 1 and loaded[0].half_width == 120 and loaded[0].n0 == 5
+    raw = direct._raw.morlet
+    assert list(loaded[0].cos_coeffs[:2 * raw.n_cos]) == list(raw.cos_coeffs[:2 * raw.n_cos])
+    assert list(loaded[0].sin_coeffs[:2 * raw.n_sin]) == list(raw.sin_coeffs[:2 * raw.n_sin])
+    again = sft.morlet_direct_spec_from_coeffs(loaded[0], sft.Precision.Double, sft.Strategy.Recursive2, True)
+    assert again.ps == direct.ps and again.pd == 6 and again.n0 == 5 and again.alpha == direct.alpha
+    assert abs(again.kernel_rmse_percent - direct.kernel_rmse_percent) < 1e-12
+    bad = tmp_path / "bad.coef"
+    bad.write_text("not a header\n")
+    with pytest.raises(ValueError):
+        sft.read_coefficient_sets(str(bad))
+
+
+def test_scalogram_coefficient_cache_matches_fresh_fits(sft):
+    """The committed 128-scale coefficient cache equals fresh fits (spot check)."""
+    import os
+
+    from paper_2110_11866_b200 import scalogram as SG
+
+    cache = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2110_11866_b200",
+                         "data", "scalogram128_xi10_pd6.coef")
+    sets = sft.read_coefficient_sets(cache)
+    sig = SG.scale_sigmas()
+    assert len(sets) == 128
+    for i in (0, 40, 90):
+        fresh = sft.make_morlet_direct_spec(sig[i], 10.0, 6, SG.default_n0(sig[i]),
+                                            sft.TransformOptions(precision=sft.Precision.Single))
+        raw = fresh._raw.morlet
+        assert sets[i].n_cos == raw.n_cos and list(sets[i].cos_orders[:raw.n_cos]) == list(raw.cos_orders[:raw.n_cos])
+        assert max(abs(a - b) for a, b in zip(sets[i].cos_coeffs[:2 * raw.n_cos], raw.cos_coeffs[:2 * raw.n_cos])) < 1e-15
