@@ -101,6 +101,8 @@ struct ScanParams {
   long long total_tiles;  // LB: tiles in the grid
   long long chunk_len;    // SEQ: outputs per chunk (multiple of the tile), one CTA per chunk
   long long n_chunks;     // SEQ: chunks per signal
+  int lb_D;               // LB: full tiles in the 2K window (2K = lb_D*TT + r)
+  int lb_sfx;             // LB: first position of a tile's r-position suffix (TT if r == 0)
   // ctrl[0] ticket, ctrl[1] finished-CTA count, ctrl[2] launch epoch. The last CTA
   // of a launch resets ticket/count and bumps the epoch, so launches need no host
   // state (graph-capturable) and stale look-back flags are ignored.
@@ -164,6 +166,15 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 }
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 
+__device__ __forceinline__ double2 warp_sum2(double2 v) {
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, d);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, d);
+  }
+  return v;
+}
+
 template <typename T2>
 __device__ __forceinline__ T2 make2(decltype(T2::x) a, decltype(T2::x) b) {
   T2 r;
@@ -212,81 +223,57 @@ struct Smem {
   T trail[2][PAD];
   T2 w[NW][NORD];         // warp totals, then per-warp carries
   double2 carry[NORD];    // state at the end of the previous tile (fp64)
-  double2 tagg[NORD];     // this tile's aggregate
-  double2 pay[32][NORD];  // look-back payload staging
+  double2 tagg[NORD];     // this tile's aggregate (SEQ) / lead-only aggregate (LB)
+  double2 tsfx[NORD];     // LB: lead-only aggregate of the tile's last r positions
+  T2 wla[NW][NORD];       // LB: per-warp lead-only totals
+  T2 wsa[NW][NORD];       // LB: per-warp lead-only suffix totals
+  union {                 // disjoint lifetimes: warp scan, then look-back
+    T2 wscan[NW][NORD * 33];  // per-warp transposed scan staging (padded)
+    double2 pay[64][NORD];    // look-back payload staging (64 predecessors per round)
+  };
   long long tile;
   unsigned int epoch;
 };
 
-// Decoupled look-back over tiles (warp 0 of an LB-mode CTA). Publishes the tile
-// aggregate, resolves the carry (state at the end of the previous tile) from the
-// predecessors' aggregates / inclusive prefixes, publishes the inclusive prefix.
-// Flags: (epoch << 32) | status, status 1 = aggregate, 2 = inclusive.
+// LB-mode carry (warp 0). The window state depends only on the last 2K leading
+// samples, V[n] = sum_{m=n-2K+1}^{n} z^{n-m} x[m+K], so the carry into tile t is the
+// finite sum  sum_{d=1}^{D} z^{TT(d-1)} LA_{t-d} + z^{TT D} SA_{t-D-1}  of the
+// predecessors' lead-only aggregates (LA: whole tile, SA: its last r positions).
+// Every tile publishes (LA, SA) as soon as its samples are staged; nothing waits on a
+// chain of inclusive prefixes. Flags: (epoch << 32) | 1, payload LA in `agg`, SA in
+// `incl`. Staged 64 predecessors per round, Horner from the oldest (fp64).
 template <typename T, int NORD, int L, int NT>
-__device__ __forceinline__ void lookback(const ScanParams<T>& P, Smem<T, NORD, L, NT>& S, long long gt,
-                                         long long first, int lane) {
-  const unsigned long long ep = static_cast<unsigned long long>(S.epoch) << 32;
-  if (gt == first) {
-    if (lane < NORD) {
-      P.incl[gt * NORD + lane] = S.tagg[lane];
-      S.carry[lane] = make_double2(0.0, 0.0);
-    }
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence();
-      st_release_u64(P.flags + gt, ep | 2ull);
-    }
-    __syncwarp();
-    return;
-  }
-  if (lane < NORD) P.agg[gt * NORD + lane] = S.tagg[lane];
-  __syncwarp();
-  if (lane == 0) {
-    __threadfence();
-    st_release_u64(P.flags + gt, ep | 1ull);
-  }
-  double2 run = make_double2(0.0, 0.0), scl = make_double2(1.0, 0.0);
+__device__ __forceinline__ void window_carry(const ScanParams<T>& P, Smem<T, NORD, L, NT>& S, long long gt,
+                                             long long first, int lane) {
+  double2 acc = make_double2(0.0, 0.0);
   const double2 zT = lane < NORD ? P.tab_tile[lane * 2] : make_double2(1.0, 0.0);
-  const double2 z32T = lane < NORD ? P.tab_tile[lane * 2 + 1] : make_double2(1.0, 0.0);
-  long long base = gt - 1;
-  while (true) {
-    const long long t = base - lane;
-    int st = 3;  // 3: before the signal's first tile = inclusive zero
-    if (t >= first) {
-      do {
-        const unsigned long long f = ld_acquire_u64(P.flags + t);
-        st = (static_cast<unsigned int>(f >> 32) == S.epoch) ? static_cast<int>(f & 3ull) : 0;
-      } while (st == 0);
-    }
-    const unsigned inc = __ballot_sync(0xffffffffu, st >= 2);
-    const int m = inc ? __ffs(inc) - 1 : 31;
-    if (lane <= m) {
-      const double2* src = (st == 2) ? P.incl : P.agg;
+  for (int hi = P.lb_D + 1; hi >= 1; hi -= 64) {
+    const int lo_d = hi - 63 > 1 ? hi - 63 : 1;
+    const int cnt = hi - lo_d + 1;
 #pragma unroll
-      for (int p = 0; p < NORD; ++p)
-        S.pay[lane][p] = (st == 3) ? make_double2(0.0, 0.0) : __ldcg(src + t * NORD + p);
+    for (int k = 0; k < 2; ++k) {
+      const int j = lane + 32 * k;
+      if (j < cnt) {
+        const int d = hi - j;
+        const long long t = gt - d;
+        if (t < first) {
+#pragma unroll
+          for (int p = 0; p < NORD; ++p) S.pay[j][p] = make_double2(0.0, 0.0);
+        } else {
+          while ((static_cast<unsigned int>(ld_acquire_u64(P.flags + t) >> 32)) != S.epoch) {
+          }
+          const double2* src = (d == P.lb_D + 1) ? P.incl : P.agg;
+#pragma unroll
+          for (int p = 0; p < NORD; ++p) S.pay[j][p] = __ldcg(src + t * NORD + p);
+        }
+      }
     }
     __syncwarp();
-    if (lane < NORD) {
-      // acc = sum_{l<=m} z^{TT l} v_l by Horner from the oldest tile
-      double2 acc = S.pay[m][lane];
-      for (int l = m - 1; l >= 0; --l) acc = cadd(cmul(acc, zT), S.pay[l][lane]);
-      run = cadd(run, cmul(scl, acc));
-      scl = cmul(scl, z32T);
-    }
+    if (lane < NORD)
+      for (int j = 0; j < cnt; ++j) acc = cadd(cmul(acc, zT), S.pay[j][lane]);
     __syncwarp();
-    if (inc) break;
-    base -= 32;
   }
-  if (lane < NORD) {
-    S.carry[lane] = run;
-    P.incl[gt * NORD + lane] = cadd(cmul(zT, run), S.tagg[lane]);
-  }
-  __syncwarp();
-  if (lane == 0) {
-    __threadfence();
-    st_release_u64(P.flags + gt, ep | 2ull);
-  }
+  if (lane < NORD) S.carry[lane] = acc;
   __syncwarp();
 }
 
@@ -358,6 +345,12 @@ struct Cx<float> {
   static __device__ __forceinline__ S shfl_up(S v, int d) {
     return pk(__shfl_up_sync(0xffffffffu, re(v), d), __shfl_up_sync(0xffffffffu, im(v), d));
   }
+  static __device__ __forceinline__ S warp_sum(S v) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1)
+      v = fma2(pk(1.0f, 1.0f), pk(__shfl_xor_sync(0xffffffffu, re(v), d), __shfl_xor_sync(0xffffffffu, im(v), d)), v);
+    return v;
+  }
 };
 
 template <>
@@ -391,6 +384,7 @@ struct Cx<double> {
   static __device__ __forceinline__ S shfl_up(S v, int d) {
     return make_double2(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
   }
+  static __device__ __forceinline__ S warp_sum(S v) { return warp_sum2(v); }
 };
 
 // One tile: stage samples, phase 1, scans, carry (SEQ: from smem; LB: look-back),
@@ -422,6 +416,54 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
   }
   __syncthreads();
   if (has_next) fetch_tile<T, L, NT>(P, xs, lo, o0 + TT, tid, fl, ft);  // in flight during this tile
+
+  if constexpr (!SEQ) {
+    // ---- lead-only aggregates (whole tile and its last r positions), published for
+    // the successors' window carries
+#pragma unroll
+    for (int p = 0; p < NORD; ++p) {
+      const OrdConst<T>& c = P.oc[p];
+      St la = X::zero(), sa = X::zero();
+#pragma unroll
+      for (int i = 0; i < L; ++i) {
+        const int e = tid * L + i;
+        const T xl = sl[e + (e >> 5)];
+        la = X::agg_r(c, i, xl, la);
+        sa = X::agg_r(c, i, e >= P.lb_sfx ? xl : T(0), sa);
+      }
+      const T* rot = P.tab + (p * kTabStride + 31 - lane) * 4;  // z^{L(31-lane)}
+      la = X::warp_sum(X::madd(rot, la, X::zero()));
+      sa = X::warp_sum(X::madd(rot, sa, X::zero()));
+      if (lane == 0) {
+        S.wla[warp][p] = make2<T2>(X::re(la), X::im(la));
+        S.wsa[warp][p] = make2<T2>(X::re(sa), X::im(sa));
+      }
+    }
+    __syncthreads();
+    if (tid < NORD) {
+      const int p = tid;
+      St a = X::zero(), b2 = X::zero();
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        a = X::madd(P.oc[p].m32, a, X::make(S.wla[w][p].x, S.wla[w][p].y));
+        b2 = X::madd(P.oc[p].m32, b2, X::make(S.wsa[w][p].x, S.wsa[w][p].y));
+      }
+      S.tagg[p] = make_double2(static_cast<double>(X::re(a)), static_cast<double>(X::im(a)));
+      S.tsfx[p] = make_double2(static_cast<double>(X::re(b2)), static_cast<double>(X::im(b2)));
+    }
+    if (warp == 0) {
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int p = 0; p < NORD; ++p) {
+          __stcg(P.agg + gt * NORD + p, S.tagg[p]);
+          __stcg(P.incl + gt * NORD + p, S.tsfx[p]);
+        }
+        st_release_u64(P.flags + gt, (static_cast<unsigned long long>(S.epoch) << 32) | 1ull);
+      }
+    }
+    if (warm) return;  // warm tiles only feed their successors' windows
+  }
 
   // ---- injections, shared across orders where the group mode allows
   T xt_[L];
@@ -463,20 +505,31 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
     st[p] = acc;
   }
 
-  // ---- warp inclusive scan of (z^{L*d}, state) pairs, then exclusive
+  // ---- warp-level exclusive scan, transposed: every thread parks its per-order
+  // aggregates in shared memory, then lane p runs the 32-step Horner chain for order p
+  // (padded stride 33: conflict-free), writing each lane's exclusive prefix in place.
+  {
+    T2* wa = S.wscan[warp];
 #pragma unroll
-  for (int p = 0; p < NORD; ++p) {
-    St v = st[p];
-
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      const int d = 1 << k;
-      const St u = X::shfl_up(v, d);
-      if (lane >= d) v = X::madd(P.oc[p].scan[k], u, v);
+    for (int p = 0; p < NORD; ++p) wa[p * 33 + lane] = make2<T2>(X::re(st[p]), X::im(st[p]));
+    __syncwarp();
+    if (lane < NORD) {
+      const T* zl = P.oc[lane].scan[0];  // z^L
+      St run = X::zero();
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) {
+        const T2 a = wa[lane * 33 + j];
+        wa[lane * 33 + j] = make2<T2>(X::re(run), X::im(run));
+        run = X::madd(zl, run, X::make(a.x, a.y));
+      }
+      S.w[warp][lane] = make2<T2>(X::re(run), X::im(run));
     }
-    if (lane == 31) S.w[warp][p] = make2<T2>(X::re(v), X::im(v));
-    const St u = X::shfl_up(v, 1);
-    st[p] = lane ? u : X::zero();
+    __syncwarp();
+#pragma unroll
+    for (int p = 0; p < NORD; ++p) {
+      const T2 e = wa[p * 33 + lane];
+      st[p] = X::make(e.x, e.y);
+    }
   }
   __syncthreads();
 
@@ -492,8 +545,8 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
       const T2 t = S.w[w][p];
       run = X::madd(P.oc[p].m32, run, X::make(t.x, t.y));  // z^{32L} run + total_w
     }
-    S.tagg[p] = make_double2(static_cast<double>(X::re(run)), static_cast<double>(X::im(run)));
     if constexpr (SEQ) {
+      S.tagg[p] = make_double2(static_cast<double>(X::re(run)), static_cast<double>(X::im(run)));
       const double2 c = S.carry[p];
       const St cs = X::make(static_cast<T>(c.x), static_cast<T>(c.y));
 #pragma unroll
@@ -510,7 +563,7 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
   if constexpr (!SEQ) {
     if (warp == 0) {
       __syncwarp();
-      lookback<T, NORD, L, NT>(P, S, gt, first, lane);
+      window_carry<T, NORD, L, NT>(P, S, gt, first, lane);
       if (tid < NORD) {
         const int p = tid;
 
@@ -525,19 +578,7 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
     }
   }
   __syncthreads();
-  if constexpr (!SEQ) {
-    if (tid == 0) {
-      // every CTA of the launch has its ticket and its look-back done: the last re-arms
-      __threadfence();
-      if (atomicAdd(P.ctrl + 1, 1u) == static_cast<unsigned int>(P.total_tiles - 1)) {
-        atomicExch(P.ctrl, 0u);
-        atomicExch(P.ctrl + 1, 0u);
-        atomicAdd(P.ctrl + 2, 1u);
-        __threadfence();
-      }
-    }
-  }
-  if (warm) return;  // warm tile: phase 1 only (uniform per CTA)
+  if (warm) return;  // SEQ warm tile: phase 1 only (uniform per CTA)
 
   // state entering this thread's segment: z^{L*lane} * Cw + in-warp exclusive
 #pragma unroll
@@ -662,6 +703,13 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? 4 : 2)) sft_scan_kernel(
     if (tid == 0) {
       S.tile = static_cast<long long>(atomicAdd(P.ctrl, 1u));
       S.epoch = *reinterpret_cast<volatile unsigned int*>(P.ctrl + 2);
+      // every CTA has its ticket once the count is complete: the last one re-arms the
+      // control block (the next launch is stream-ordered after this one)
+      if (atomicAdd(P.ctrl + 1, 1u) == static_cast<unsigned int>(P.total_tiles - 1)) {
+        atomicExch(P.ctrl, 0u);
+        atomicExch(P.ctrl + 1, 0u);
+        atomicAdd(P.ctrl + 2, 1u);
+      }
     }
     __syncthreads();
     const long long gt = S.tile;

@@ -656,6 +656,11 @@ void run_groups(sftgpu_plan* pl, const void* x, long long ld_x, void* out, void*
     P.total_tiles = pl->total_tiles;
     P.chunk_len = pl->chunk_len;
     P.n_chunks = pl->n_chunks;
+    P.lb_D = static_cast<int>((2LL * pl->K) / pl->TT);
+    {
+      const long long r = 2LL * pl->K - static_cast<long long>(P.lb_D) * pl->TT;
+      P.lb_sfx = static_cast<int>(pl->TT - r);
+    }
     P.ctrl = pl->d_ctrl;
     P.flags = pl->d_flags;
     P.agg = pl->d_agg;
