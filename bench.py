@@ -52,6 +52,55 @@ def env_int(name, default):
         return default
 
 
+# ------------------------------------------------------------------ distributed helpers
+def dist_init(args, local):
+    """One process per GPU. NCCL by default; --dist-backend gloo lets a multi-rank run
+    share one GPU (used to exercise the N>1 path when only one device is available)."""
+    import torch
+    import torch.distributed as dist
+
+    world = env_int("WORLD_SIZE", 1)
+    if world > 1:
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    return world
+
+
+def device_index(args, local):
+    return 0 if args.share_device else local
+
+
+def max_over_ranks(value: float, world: int) -> float:
+    """Max of a host scalar over ranks (CPU tensor: works with NCCL and gloo)."""
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend() == "nccl":
+        t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    else:
+        t = torch.tensor([value], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def broadcast_tensor(x, world: int):
+    if world == 1:
+        return x
+    import torch.distributed as dist
+
+    if dist.get_backend() == "nccl":
+        dist.broadcast(x, src=0)
+        return x
+    h = x.cpu()
+    dist.broadcast(h, src=0)
+    x.copy_(h)
+    return x
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """Samples SM clocks and throttle reasons via NVML while the timed region runs."""
@@ -194,10 +243,9 @@ def run_ours(args, w, spec_of):
 
     import paper_2110_11866_b200 as P
 
-    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, local = env_int("RANK", 0), env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(device_index(args, local))
+    world = dist_init(args, device_index(args, local))
 
     spec = spec_of()
     n, batch = w["n"], w["batch"]
@@ -244,7 +292,7 @@ def run_ours(args, w, spec_of):
                 dist.barrier()
             return ev0.elapsed_time(ev1)
 
-        with ClockSampler(local) as clk:
+        with ClockSampler(device_index(args, local)) as clk:
             ms = timed_region()
             # keep the clock record meaningful for sub-second regions: sample a few more
             # identical replays (not part of the reported number) only if too few samples
@@ -252,10 +300,7 @@ def run_ours(args, w, spec_of):
             while len(clk.samples) < 20 and time.perf_counter() - t_extra < 2.0 and graph is not None:
                 graph.replay()
                 stream.synchronize()
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = max_over_ranks(ms, world)
     ms_per_step = ms / args.steps
     samples = n * batch * args.steps * world
     value = samples / (ms * 1e-3) / 1e6
@@ -273,10 +318,7 @@ def run_ours(args, w, spec_of):
         for _ in range(e2e_steps):
             plan.execute_host(x_host.numpy(), o_host.numpy(), stream.cuda_stream)
         e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = n * batch * e2e_steps * world / float(te.item()) / 1e6
+    e2e_value = n * batch * e2e_steps * world / max_over_ranks(e2e_s, world) / 1e6
 
     peak, peak_src = measured_peaks()
     launches = plan.launches
@@ -335,18 +377,16 @@ def run_scalogram(args):
     import paper_2110_11866_b200 as P
     from paper_2110_11866_b200 import scalogram as SG
 
-    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, local = env_int("RANK", 0), env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(device_index(args, local))
+    world = dist_init(args, device_index(args, local))
     n, ns = args.scalogram_n, args.scalogram_scales
     cache = os.path.join(ROOT, "paper_2110_11866_b200", "data", f"scalogram{ns}_xi10_pd6.coef")
     specs = SG.build_specs(SG.scale_sigmas(ns), xi=10.0, pd=6, cache=cache)
     x = torch.empty(n, dtype=torch.float32, device="cuda")
     if rank == 0:
         x.copy_(P.generate_signals(P.TestSignalKind.SeededNoise, n, 1234, 1, P.Precision.Single)[0])
-    if world > 1:
-        dist.broadcast(x, src=0)
+    broadcast_tensor(x, world)
     sc = SG.Scalogram(n, specs, world, rank, args.shard)
     out = sc.empty_output()
     stream = torch.cuda.Stream()
@@ -355,7 +395,7 @@ def run_scalogram(args):
             sc.run(x, out)
         stream.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with ClockSampler(local) as clk:
+        with ClockSampler(device_index(args, local)) as clk:
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
@@ -367,14 +407,11 @@ def run_scalogram(args):
             if world > 1:
                 dist.barrier()
         ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = max_over_ranks(ms, world)
     value = n * ns * args.steps / (ms * 1e-3) / 1e6
     # final gather to rank 0 (optional, timed separately)
     gather_ms = None
-    if world > 1 and args.gather:
+    if world > 1 and args.gather and dist.get_backend() == "nccl":
         torch.cuda.synchronize()
         dist.barrier()
         g0 = time.perf_counter()
@@ -394,10 +431,7 @@ def run_scalogram(args):
         sc.run(xd, out)
         oh.copy_(out, non_blocking=True)
         stream.synchronize()
-    te = torch.tensor([time.perf_counter() - e0], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = n * ns / float(te.item()) / 1e6
+    e2e_value = n * ns / max_over_ranks(time.perf_counter() - e0, world) / 1e6
     peak, peak_src = measured_peaks()
     launches_per_step = sc.launches
     kernel_ms = ms / args.steps / max(1, launches_per_step)
@@ -441,6 +475,9 @@ def main():
     ap.add_argument("--scalogram-scales", type=int, default=128)
     ap.add_argument("--shard", choices=["scale", "chunk"], default="scale")
     ap.add_argument("--gather", action="store_true")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl")
+    ap.add_argument("--share-device", action="store_true",
+                    help="all ranks on cuda:0 (with --dist-backend gloo): exercises the N>1 path on one GPU")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

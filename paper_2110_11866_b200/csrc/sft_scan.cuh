@@ -213,24 +213,23 @@ __device__ __forceinline__ u64 cmadd2(float wr, float wi, u64 u, u64 v) {
   return fma2(pk(-wi, wi), pswap(u), fma2(pk(wr, wr), u, v));
 }
 
-template <typename T, int NORD, int L, int NT>
+template <typename T, int NORD, int L, int NT, bool SEQ>
 struct Smem {
   using T2 = typename Vec2<T>::t;
   static constexpr int TT = NT * L;
   static constexpr int PAD = TT + TT / 32;
   static constexpr int NW = NT / 32;
-  T lead[2][PAD];  // double-buffered sample staging (tile parity)
-  T trail[2][PAD];
+  static constexpr int NB = SEQ ? 2 : 1;  // SEQ double-buffers by tile parity
+  T lead[NB][PAD];
+  T trail[NB][PAD];
   T2 w[NW][NORD];         // warp totals, then per-warp carries
   double2 carry[NORD];    // state at the end of the previous tile (fp64)
   double2 tagg[NORD];     // this tile's aggregate (SEQ) / lead-only aggregate (LB)
   double2 tsfx[NORD];     // LB: lead-only aggregate of the tile's last r positions
   T2 wla[NW][NORD];       // LB: per-warp lead-only totals
   T2 wsa[NW][NORD];       // LB: per-warp lead-only suffix totals
-  union {                 // disjoint lifetimes: warp scan, then look-back
-    T2 wscan[NW][NORD * 33];  // per-warp transposed scan staging (padded)
-    double2 pay[64][NORD];    // look-back payload staging (64 predecessors per round)
-  };
+  T2 wscan[NW][NORD * 33];          // per-warp transposed scan staging (padded)
+  double2 pay[SEQ ? 1 : 64][NORD];  // LB window-carry staging (64 predecessors per round)
   long long tile;
   unsigned int epoch;
 };
@@ -242,8 +241,8 @@ struct Smem {
 // Every tile publishes (LA, SA) as soon as its samples are staged; nothing waits on a
 // chain of inclusive prefixes. Flags: (epoch << 32) | 1, payload LA in `agg`, SA in
 // `incl`. Staged 64 predecessors per round, Horner from the oldest (fp64).
-template <typename T, int NORD, int L, int NT>
-__device__ __forceinline__ void window_carry(const ScanParams<T>& P, Smem<T, NORD, L, NT>& S, long long gt,
+template <typename T, int NORD, int L, int NT, bool SEQ>
+__device__ __forceinline__ void window_carry(const ScanParams<T>& P, Smem<T, NORD, L, NT, SEQ>& S, long long gt,
                                              long long first, int lane) {
   double2 acc = make_double2(0.0, 0.0);
   const double2 zT = lane < NORD ? P.tab_tile[lane * 2] : make_double2(1.0, 0.0);
@@ -391,7 +390,7 @@ struct Cx<double> {
 // phase 2, stores. `fl/ft` hold this tile's prefetched samples on entry and the next
 // tile's on exit when `has_next`.
 template <typename T, int NORD, int NA, int GM, int MODE, int L, int NT, bool SEQ>
-__device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L, NT>& S, long long sig,
+__device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L, NT, SEQ>& S, long long sig,
                                         long long gt, long long first, long long lo, long long count,
                                         long long obase, long long o0, T (&fl)[L], T (&ft)[L],
                                         const T* __restrict__ xs, bool has_next) {
@@ -563,7 +562,7 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
   if constexpr (!SEQ) {
     if (warp == 0) {
       __syncwarp();
-      window_carry<T, NORD, L, NT>(P, S, gt, first, lane);
+      window_carry<T, NORD, L, NT, SEQ>(P, S, gt, first, lane);
       if (tid < NORD) {
         const int p = tid;
 
@@ -679,7 +678,7 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? 4 : 2)) sft_scan_kernel(
   static_assert(NORD >= 1 && NORD <= kMaxOrd, "order count");
   static_assert(L <= kMaxL, "positions per thread");
   constexpr int TT = NT * L;
-  __shared__ Smem<T, NORD, L, NT> S;
+  __shared__ Smem<T, NORD, L, NT, SEQ> S;
   const int tid = threadIdx.x;
   T fl[L], ft[L];
 
