@@ -37,6 +37,9 @@
 
 namespace sftk {
 
+#ifndef SFTK_SEQ_MINB
+#define SFTK_SEQ_MINB 4
+#endif
 constexpr int kMaxOrd = 12;
 constexpr int kMaxL = 8;
 constexpr int kTabStride = 64;  // table entries per order (see layout below)
@@ -609,40 +612,31 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
     }
   } else {
     constexpr bool CPLX = MODE == kModeComplex;
-    St acc[CPLX ? L : 1];
-    T accr[CPLX ? 1 : L];
+    constexpr int CW = CPLX ? 2 : 1;  // T words per output
+    T buf[L * CW];
+    // positions outer, orders inner: NORD independent recurrence chains per position
+    // (same per-output accumulation order as orders-outer, so results are identical)
 #pragma unroll
     for (int i = 0; i < L; ++i) {
-      if constexpr (CPLX)
-        acc[i] = X::make(P.Dr * xt_[i], P.Di * xt_[i]);
-      else
-        accr[i] = P.Dr * xt_[i];
-    }
+      St acc = X::make(P.Dr * xt_[i], CPLX ? P.Di * xt_[i] : T(0));
+      T accr = P.Dr * xt_[i];
 #pragma unroll
-    for (int p = 0; p < NORD; ++p) {
-      const OrdConst<T>& c = P.oc[p];
-      St v = st[p];
-#pragma unroll
-      for (int i = 0; i < L; ++i) {
-        v = X::step(c, v, inj(c, p, i, true));
+      for (int p = 0; p < NORD; ++p) {
+        const OrdConst<T>& c = P.oc[p];
+        st[p] = X::step(c, st[p], inj(c, p, i, true));
         if constexpr (CPLX)
-          acc[i] = X::comb(c, v, acc[i]);
+          acc = X::comb(c, st[p], acc);
         else
-          accr[i] = X::comb_re(c, v, accr[i]);
+          accr = X::comb_re(c, st[p], accr);
+      }
+      if constexpr (CPLX) {
+        buf[2 * i] = X::re(acc);
+        buf[2 * i + 1] = X::im(acc);
+      } else {
+        buf[i] = accr;
       }
     }
     // ---- stores: L consecutive outputs per thread, 16-byte vectors when aligned
-    constexpr int CW = CPLX ? 2 : 1;  // T words per output
-    T buf[L * CW];
-#pragma unroll
-    for (int i = 0; i < L; ++i) {
-      if constexpr (CPLX) {
-        buf[2 * i] = X::re(acc[i]);
-        buf[2 * i + 1] = X::im(acc[i]);
-      } else {
-        buf[i] = accr[i];
-      }
-    }
     T* optr = P.out + CW * (sig * P.ld_out + obase);
     constexpr int VW = 16 / sizeof(T);  // T words per 16-byte vector
     if (P.vec_ok && !P.accumulate && ob + L <= count && (L * CW) % VW == 0) {
@@ -674,7 +668,7 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
 }
 
 template <typename T, int NORD, int NA, int GM, int MODE, int L, int NT, bool SEQ>
-__global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? 4 : 2)) sft_scan_kernel(const __grid_constant__ ScanParams<T> P) {
+__global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? SFTK_SEQ_MINB : 4) : 2)) sft_scan_kernel(const __grid_constant__ ScanParams<T> P) {
   static_assert(NORD >= 1 && NORD <= kMaxOrd, "order count");
   static_assert(L <= kMaxL, "positions per thread");
   constexpr int TT = NT * L;
