@@ -412,3 +412,72 @@ def test_chunked_sequential_matches_lookback(sft, O, abbrev, sigma, xi, prec, to
     ref = oracle_transform(O, xh, 1, spec)
     got = outs["seq"][..., 0] + 1j * outs["seq"][..., 1] if outs["seq"].ndim == 2 else outs["seq"]
     assert rel_max(got, ref) < (1e-5 if prec == 0 else 1e-12)
+
+
+@pytest.mark.parametrize("mode", ["lookback", "seq"])
+@pytest.mark.parametrize("prec,tol", [(0, 1e-5), (1, 1e-12)])
+@pytest.mark.parametrize("boundary", [0, 1])
+def test_split_launches_modes_boundaries(sft, O, mode, prec, tol, boundary):
+    """17 orders (MMS5P5: 11 real-frequency + 6 kappa orders) run as two accumulating
+    launches; both execution modes, both precisions and both boundary policies agree
+    with the oracle."""
+    import torch
+
+    spec = sft.make_transform_spec("MMS5P5", 60.0, 10.0, sft.TransformOptions(precision=prec))
+    n = 20011
+    x = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 3, 2, sft.Precision(prec))
+    plan = sft.TransformPlan(spec, n, 2, boundary, mode=mode)
+    assert plan.launches == 2
+    out = plan.empty_output()
+    plan.execute(x, out)
+    torch.cuda.synchronize()
+    xh = x.double().cpu().numpy()
+    oh = out.double().cpu().numpy()
+    for b in range(2):
+        ref = oracle_transform(O, xh[b], boundary, spec)
+        assert rel_max(oh[b, :, 0] + 1j * oh[b, :, 1], ref) < tol
+
+
+@pytest.mark.parametrize("prec,tol", [(0, 1e-5), (1, 1e-12)])
+def test_sequential_ranged_plans(sft, O, prec, tol):
+    """Ranged plans in sequential (chunked) mode: each output chunk starts its own warm-up
+    inside the range and still matches the full-signal oracle."""
+    import torch
+
+    spec = sft.make_transform_spec("GDS3P6", 50.0, 0.0, sft.TransformOptions(precision=prec))
+    n = 400009
+    x = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 21, 1, sft.Precision(prec))
+    ref = oracle_transform(O, x[0].double().cpu().numpy(), 1, spec).real
+    for b, c in ((0, 150000), (150000, 250009), (333, 7)):
+        p = sft.TransformPlan(spec, n, 1, sft.BoundaryPolicy.Clamp, (b, c), mode="seq")
+        o = p.empty_output()
+        p.execute(x, o)
+        torch.cuda.synchronize()
+        assert rel_max(o[0].double().cpu().numpy(), ref[b:b + c]) < tol
+
+
+def test_plan_reuse_and_graph_capture(sft, O):
+    """Plans carry no host-side per-launch state: repeated executes and CUDA-graph
+    replays give identical results."""
+    import torch
+
+    spec = sft.make_transform_spec("MDS5P6", 512.0, 10.0, sft.TransformOptions(precision=0))
+    n = 50000
+    x = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 8, 1, sft.Precision.Single)
+    plan = sft.TransformPlan(spec, n)
+    o1, o2 = plan.empty_output(), plan.empty_output()
+    plan.execute(x, o1)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        plan.execute(x, o2)  # warm on the capture stream
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        o2.zero_()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(3):
+                plan.execute(x, o2)
+        for _ in range(4):
+            g.replay()
+        s.synchronize()
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
