@@ -272,6 +272,16 @@ int sftgpu_generate_signal(int kind, int64_t n, uint64_t seed, int64_t batch, in
 int sftgpu_truncated_convolution(const double* x, int64_t n, int boundary,
                                  const double* taps, int64_t n_taps, int64_t tap_lo,
                                  double* out, void* stream);
+/* The paper's data-parallel sliding sum h[n] = sum_{k<L} f[n+k], n in [0, N-L]
+ * (sliding_sum_flat / sliding_sum_blocked8, include/sft/sliding_sum.hpp:89-234): Algorithm 1
+ * (flat doubling) or Algorithms 2-3 (blocked8, (16,8) tiles) as GPU kernels with the reference's
+ * exact addition trees (bit-identical for int64 and fp64). Device buffers; synchronous.
+ * info (plan + cost model, src/sliding_sum.cpp:7-40): {rounds R, padded size, blocked stages,
+ * parallel steps, total adds}. */
+enum { SFTGPU_SS_I64 = 0, SFTGPU_SS_F64 = 1, SFTGPU_SS_C128 = 2 };
+int sftgpu_sliding_sum_plan(int64_t n, int64_t L, int blocked, int64_t* info);
+int sftgpu_sliding_sum(int dtype, int blocked, const void* f, int64_t n, int64_t L, void* out, void* stream);
+
 /* Host-memory variants (device buffers managed internally; synchronous). */
 int sftgpu_generate_signal_host(int kind, int64_t n, uint64_t seed, double* out_host);
 int sftgpu_truncated_convolution_host(const double* x_host, int64_t n, int boundary,

@@ -138,6 +138,8 @@ SIGNATURES = {
     "sftgpu_plan_destroy": ([_P], None),
     "sftgpu_generate_signal_host": ([_I, _I64, _U64, _P], _I),
     "sftgpu_truncated_convolution_host": ([_P, _I64, _I, _P, _I64, _I64, _P], _I),
+    "sftgpu_sliding_sum_plan": ([_I64, _I64, _I, C.POINTER(C.c_int64)], _I),
+    "sftgpu_sliding_sum": ([_I, _I, _P, _I64, _I64, _P, _P], _I),
     "sftgpu_generate_signal": ([_I, _I64, _U64, _I64, _I, _P, _P], _I),
     "sftgpu_truncated_convolution": ([_P, _I64, _I, _P, _I64, _I64, _P, _P], _I),
 }

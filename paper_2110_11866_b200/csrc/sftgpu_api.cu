@@ -16,9 +16,10 @@
 #include "scan_launch.cuh"
 
 namespace {
-
 using cd = std::complex<double>;
+}  // namespace
 thread_local std::string g_err;
+namespace {
 
 struct ApiError {
   int code;
@@ -702,6 +703,8 @@ void run_conv(sftgpu_plan* pl, const void* x, long long ld_x, void* out, long lo
 }
 
 }  // namespace
+
+void sftgpu_set_error(const std::string& m) { g_err = m; }
 
 extern "C" {
 

@@ -30,7 +30,7 @@ __all__ = [
     "fit_mmse", "select_optimal_ps", "tune_beta_gauss", "gauss_kernel_rmse",
     "morlet_direct_kernel_rmse", "morlet_multiply_kernel_rmse", "TransformPlan", "ComponentsPlan",
     "FitDegenerateError", "SftGpuError", "write_coefficient_sets", "read_coefficient_sets",
-    "morlet_direct_spec_from_coeffs",
+    "morlet_direct_spec_from_coeffs", "sliding_sum_plan", "sliding_sum_flat", "sliding_sum_blocked8",
 ]
 
 
@@ -425,6 +425,45 @@ def morlet_direct_spec_from_coeffs(raw: "_abi.Coeffs", precision=Precision.Doubl
     check(lib().sftgpu_make_morlet_direct_spec_from_coeffs(C.byref(raw), int(precision), int(strategy),
                                                            int(recompute_rmse), C.byref(spec)))
     return TransformSpec(spec)
+
+
+def sliding_sum_plan(n: int, window: int, blocked: bool = False) -> dict:
+    """SlidingSumPlan::make + cost_model (proj/include/sft/sliding_sum.hpp:32-60,
+    proj/src/sliding_sum.cpp:7-40)."""
+    info = (C.c_int64 * 5)()
+    check(lib().sftgpu_sliding_sum_plan(n, window, int(blocked), info))
+    keys = ("rounds", "padded_size", "blocked_stages", "parallel_steps", "total_adds")
+    return dict(zip(keys, list(info)))
+
+
+def _sliding(f, window: int, blocked: bool):
+    torch = _torch()
+    a = np.ascontiguousarray(np.asarray(f))
+    if a.dtype == np.int64:
+        dt, code = torch.int64, 0
+    elif np.iscomplexobj(a):
+        a = a.astype(np.complex128)
+        dt, code = torch.complex128, 2
+    else:
+        a = a.astype(np.float64)
+        dt, code = torch.float64, 1
+    n = a.size
+    x = torch.from_numpy(a).to("cuda")
+    out = torch.empty(max(1, n - window + 1), dtype=dt, device="cuda")
+    check(lib().sftgpu_sliding_sum(code, int(blocked), C.c_void_p(x.data_ptr()), n, window,
+                                   C.c_void_p(out.data_ptr()), _stream_ptr(torch)))
+    return out.cpu().numpy()
+
+
+def sliding_sum_flat(f, window: int, workers: int = 1):
+    """Algorithm 1 on the GPU (proj/include/sft/sliding_sum.hpp:89-121): h[n] = sum_{k<L} f[n+k],
+    same addition tree as the reference (bit-identical for int64 / float64)."""
+    return _sliding(f, window, False)
+
+
+def sliding_sum_blocked8(f, window: int, workers: int = 1):
+    """Algorithms 2-3 on the GPU ((16,8) shared-memory tiles, proj/include/sft/sliding_sum.hpp:144-234)."""
+    return _sliding(f, window, True)
 
 
 @dataclass
