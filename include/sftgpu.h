@@ -237,6 +237,19 @@ int sftgpu_transform_execute(sftgpu_plan* plan, const void* x, int64_t ld_x, voi
  * pinned memory recommended). Synchronises `stream` before returning. */
 int sftgpu_transform_execute_host(sftgpu_plan* plan, const void* x_host, void* out_host,
                                   void* stream);
+/* Pipelined variant for streams of host buffers: enqueues H2D of x_host, the transform
+ * and D2H into out_host on the plan's internal copy-in / compute / copy-out streams
+ * (three staging slots) and returns without waiting, so the copies of neighbouring calls
+ * overlap this call's kernel. Work queued on `stream` before the call runs first, and
+ * `stream` waits for this call's D2H: after cudaStreamSynchronize(stream) (or
+ * sftgpu_plan_synchronize) out_host holds the result. x_host must stay valid and
+ * out_host untouched until then; host buffers must be pinned for the copies to overlap.
+ * Do not interleave with sftgpu_transform_execute on the same plan while calls are in
+ * flight (they share the look-back workspace). */
+int sftgpu_transform_execute_host_async(sftgpu_plan* plan, const void* x_host, void* out_host,
+                                        void* stream);
+/* Blocks until every pipelined call on the plan has finished. */
+int sftgpu_plan_synchronize(sftgpu_plan* plan);
 /* 1 if the transform output is complex, 0 if real. */
 int sftgpu_plan_output_is_complex(const sftgpu_plan* plan);
 /* Plan geometry: info[0..7] = {sequential, direct-convolution, positions per thread,

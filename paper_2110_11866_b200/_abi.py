@@ -130,6 +130,8 @@ SIGNATURES = {
     "sftgpu_plan_describe": ([_P, C.POINTER(C.c_int64), _I], _I),
     "sftgpu_transform_execute": ([_P, _P, _I64, _P, _I64, _P], _I),
     "sftgpu_transform_execute_host": ([_P, _P, _P, _P], _I),
+    "sftgpu_transform_execute_host_async": ([_P, _P, _P, _P], _I),
+    "sftgpu_plan_synchronize": ([_P], _I),
     "sftgpu_plan_output_is_complex": ([_P], _I),
     "sftgpu_plan_launches_per_execute": ([_P], _I),
     "sftgpu_components_plan_create": ([C.POINTER(Config), _I, _I64, _I64, _I, _I64, _I64, _I, C.POINTER(_P)], _I),

@@ -123,8 +123,36 @@ struct sftgpu_plan {
   void* d_out = nullptr;
   size_t cap_x = 0, cap_out = 0;
   int device = 0;
+  // pipelined host execution: internal copy-in / compute / copy-out streams and a ring
+  // of staging slots, so the transfers of neighbouring calls overlap this call's kernel
+  struct Slot {
+    void* d_x = nullptr;
+    void* d_out = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_comp = nullptr, ev_out = nullptr;
+  };
+  static constexpr int kSlots = 3;
+  Slot slots[kSlots];
+  cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+  cudaEvent_t ev_entry = nullptr;
+  int next_slot = 0;
 
   ~sftgpu_plan() {
+    if (s_in) {
+      cudaStreamSynchronize(s_in);
+      cudaStreamSynchronize(s_comp);
+      cudaStreamSynchronize(s_out);
+      for (Slot& sl : slots) {
+        cudaFree(sl.d_x);
+        cudaFree(sl.d_out);
+        cudaEventDestroy(sl.ev_in);
+        cudaEventDestroy(sl.ev_comp);
+        cudaEventDestroy(sl.ev_out);
+      }
+      cudaEventDestroy(ev_entry);
+      cudaStreamDestroy(s_in);
+      cudaStreamDestroy(s_comp);
+      cudaStreamDestroy(s_out);
+    }
     for (Group& g : groups) {
       cudaFree(g.d_tab);
       cudaFree(g.d_tab_tile);
@@ -991,35 +1019,93 @@ int sftgpu_transform_execute(sftgpu_plan* pl, const void* x, int64_t ld_x, void*
   });
 }
 
+namespace {
+size_t plan_in_bytes(const sftgpu_plan* pl) { return static_cast<size_t>(pl->n * pl->batch) * elem_size(pl->precision); }
+size_t plan_out_bytes(const sftgpu_plan* pl) {
+  return static_cast<size_t>(pl->count * pl->batch) * elem_size(pl->precision) * (pl->mode == sftk::kModeComplex ? 2 : 1);
+}
+void ensure_buffer(void** p, size_t* cap, size_t bytes, const char* what) {
+  if (*cap >= bytes) return;
+  cudaFree(*p);
+  *p = nullptr;
+  cuda_check(cudaMalloc(p, bytes), what);
+  *cap = bytes;
+}
+void run_transform(sftgpu_plan* pl, const void* d_x, void* d_out, cudaStream_t st) {
+  if (pl->conv) {
+    run_conv(pl, d_x, pl->n, d_out, pl->n, st);
+  } else if (pl->precision == SFTGPU_SINGLE) {
+    run_groups<float>(pl, d_x, pl->n, d_out, nullptr, pl->count, 0, st);
+  } else {
+    run_groups<double>(pl, d_x, pl->n, d_out, nullptr, pl->count, 0, st);
+  }
+}
+}  // namespace
+
 int sftgpu_transform_execute_host(sftgpu_plan* pl, const void* x_host, void* out_host, void* stream) {
   return guarded([&] {
     if (!pl || pl->is_components) fail(SFTGPU_EINVAL, "not a transform plan");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const size_t es = elem_size(pl->precision);
-    const size_t xb = static_cast<size_t>(pl->n * pl->batch) * es;
-    const size_t ob = static_cast<size_t>(pl->count * pl->batch) * es * (pl->mode == sftk::kModeComplex ? 2 : 1);
-    if (pl->cap_x < xb) {
-      cudaFree(pl->d_x);
-      pl->d_x = nullptr;
-      cuda_check(cudaMalloc(&pl->d_x, xb), "cudaMalloc staging x");
-      pl->cap_x = xb;
-    }
-    if (pl->cap_out < ob) {
-      cudaFree(pl->d_out);
-      pl->d_out = nullptr;
-      cuda_check(cudaMalloc(&pl->d_out, ob), "cudaMalloc staging out");
-      pl->cap_out = ob;
-    }
+    const size_t xb = plan_in_bytes(pl), ob = plan_out_bytes(pl);
+    ensure_buffer(&pl->d_x, &pl->cap_x, xb, "cudaMalloc staging x");
+    ensure_buffer(&pl->d_out, &pl->cap_out, ob, "cudaMalloc staging out");
     cuda_check(cudaMemcpyAsync(pl->d_x, x_host, xb, cudaMemcpyHostToDevice, st), "H2D");
-    if (pl->conv) {
-      run_conv(pl, pl->d_x, pl->n, pl->d_out, pl->n, st);
-    } else if (pl->precision == SFTGPU_SINGLE) {
-      run_groups<float>(pl, pl->d_x, pl->n, pl->d_out, nullptr, pl->count, 0, st);
-    } else {
-      run_groups<double>(pl, pl->d_x, pl->n, pl->d_out, nullptr, pl->count, 0, st);
-    }
+    run_transform(pl, pl->d_x, pl->d_out, st);
     cuda_check(cudaMemcpyAsync(out_host, pl->d_out, ob, cudaMemcpyDeviceToHost, st), "D2H");
     cuda_check(cudaStreamSynchronize(st), "stream sync");
+  });
+}
+
+int sftgpu_transform_execute_host_async(sftgpu_plan* pl, const void* x_host, void* out_host, void* stream) {
+  return guarded([&] {
+    if (!pl || pl->is_components) fail(SFTGPU_EINVAL, "not a transform plan");
+    if (!x_host || !out_host) fail(SFTGPU_EINVAL, "null host buffer");
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    if (!pl->s_in) {
+      const unsigned fl = cudaStreamNonBlocking;
+      cuda_check(cudaStreamCreateWithFlags(&pl->s_in, fl), "stream create");
+      cuda_check(cudaStreamCreateWithFlags(&pl->s_comp, fl), "stream create");
+      cuda_check(cudaStreamCreateWithFlags(&pl->s_out, fl), "stream create");
+      cuda_check(cudaEventCreateWithFlags(&pl->ev_entry, cudaEventDisableTiming), "event create");
+      for (auto& sl : pl->slots) {
+        cuda_check(cudaEventCreateWithFlags(&sl.ev_in, cudaEventDisableTiming), "event create");
+        cuda_check(cudaEventCreateWithFlags(&sl.ev_comp, cudaEventDisableTiming), "event create");
+        cuda_check(cudaEventCreateWithFlags(&sl.ev_out, cudaEventDisableTiming), "event create");
+      }
+    }
+    const size_t xb = plan_in_bytes(pl), ob = plan_out_bytes(pl);
+    auto& sl = pl->slots[pl->next_slot];
+    pl->next_slot = (pl->next_slot + 1) % sftgpu_plan::kSlots;
+    size_t cap = sl.d_x ? xb : 0, capo = sl.d_out ? ob : 0;
+    ensure_buffer(&sl.d_x, &cap, xb, "cudaMalloc async staging x");
+    ensure_buffer(&sl.d_out, &capo, ob, "cudaMalloc async staging out");
+    // work already queued on the caller's stream comes first
+    cuda_check(cudaEventRecord(pl->ev_entry, user), "event record");
+    cuda_check(cudaStreamWaitEvent(pl->s_in, pl->ev_entry, 0), "stream wait");
+    // copy-in may overwrite this slot's input once the slot's previous kernel has read it
+    cuda_check(cudaStreamWaitEvent(pl->s_in, sl.ev_comp, 0), "stream wait");
+    cuda_check(cudaMemcpyAsync(sl.d_x, x_host, xb, cudaMemcpyHostToDevice, pl->s_in), "H2D");
+    cuda_check(cudaEventRecord(sl.ev_in, pl->s_in), "event record");
+    // the kernel may overwrite this slot's output once its previous copy-out is done
+    cuda_check(cudaStreamWaitEvent(pl->s_comp, sl.ev_in, 0), "stream wait");
+    cuda_check(cudaStreamWaitEvent(pl->s_comp, sl.ev_out, 0), "stream wait");
+    run_transform(pl, sl.d_x, sl.d_out, pl->s_comp);
+    cuda_check(cudaEventRecord(sl.ev_comp, pl->s_comp), "event record");
+    cuda_check(cudaStreamWaitEvent(pl->s_out, sl.ev_comp, 0), "stream wait");
+    cuda_check(cudaMemcpyAsync(out_host, sl.d_out, ob, cudaMemcpyDeviceToHost, pl->s_out), "D2H");
+    cuda_check(cudaEventRecord(sl.ev_out, pl->s_out), "event record");
+    cuda_check(cudaStreamWaitEvent(user, sl.ev_out, 0), "stream wait");
+  });
+}
+
+int sftgpu_plan_synchronize(sftgpu_plan* pl) {
+  return guarded([&] {
+    if (!pl) fail(SFTGPU_EINVAL, "null plan");
+    if (pl->s_in) {
+      cuda_check(cudaStreamSynchronize(pl->s_in), "stream sync");
+      cuda_check(cudaStreamSynchronize(pl->s_comp), "stream sync");
+      cuda_check(cudaStreamSynchronize(pl->s_out), "stream sync");
+    }
   });
 }
 

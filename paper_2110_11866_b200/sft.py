@@ -179,6 +179,7 @@ class ComponentsPlan:
         h = C.c_void_p()
         check(lib().sftgpu_components_plan_create(arr, len(cfgs), n, batch, int(boundary), lo, hi, mode, C.byref(h)))
         self._h = h
+        self._destroy = lib().sftgpu_plan_destroy
         self.n_orders, self.n, self.batch, self.count = len(cfgs), n, batch, hi - lo + 1
         self.precision = Precision(cfgs[0].precision)
 
@@ -188,8 +189,10 @@ class ComponentsPlan:
         check(lib().sftgpu_components_execute(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(c.data_ptr()), C.c_void_p(s.data_ptr()), st))
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib().sftgpu_plan_destroy(self._h)
+        # the destroy entry point is bound at creation: module globals may already be
+        # torn down when this runs at interpreter exit
+        if getattr(self, "_h", None) and getattr(self, "_destroy", None):
+            self._destroy(self._h)
             self._h = None
 
 
@@ -568,6 +571,7 @@ class TransformPlan:
         check(lib().sftgpu_transform_plan_create_ex(C.byref(spec._raw), n, batch, int(boundary), begin, count,
                                                     self.MODES[mode], C.byref(h)))
         self._h = h
+        self._destroy = lib().sftgpu_plan_destroy
         self.n, self.batch, self.out_begin, self.count = n, batch, begin, count
         self.complex_out = bool(lib().sftgpu_plan_output_is_complex(h))
         conv = spec.kind in (TransformKind.TruncConvGauss, TransformKind.TruncConvMorlet)
@@ -602,9 +606,22 @@ class TransformPlan:
         check(lib().sftgpu_transform_execute_host(self._h, x_host.ctypes.data_as(C.c_void_p),
                                                   out_host.ctypes.data_as(C.c_void_p), st))
 
+    def execute_host_async(self, x_host: np.ndarray, out_host: np.ndarray, stream=None):
+        """Pipelined host-buffer execution (``sftgpu_transform_execute_host_async``): returns
+        once queued; ``stream`` (default: torch's current) waits for the result copy."""
+        torch = _torch()
+        st = C.c_void_p(stream) if stream is not None else _stream_ptr(torch)
+        check(lib().sftgpu_transform_execute_host_async(self._h, x_host.ctypes.data_as(C.c_void_p),
+                                                        out_host.ctypes.data_as(C.c_void_p), st))
+
+    def synchronize(self):
+        check(lib().sftgpu_plan_synchronize(self._h))
+
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib().sftgpu_plan_destroy(self._h)
+        # the destroy entry point is bound at creation: module globals may already be
+        # torn down when this runs at interpreter exit
+        if getattr(self, "_h", None) and getattr(self, "_destroy", None):
+            self._destroy(self._h)
             self._h = None
 
 

@@ -481,3 +481,25 @@ def test_plan_reuse_and_graph_capture(sft, O):
         s.synchronize()
     torch.cuda.synchronize()
     assert torch.equal(o1, o2)
+
+
+@pytest.mark.parametrize("mode", ["lookback", "seq"])
+def test_pipelined_host_execution(sft, O, mode):
+    """sftgpu_transform_execute_host_async: a stream of distinct pinned host buffers, all
+    calls in flight before one sync, each result bit-identical to the synchronous call."""
+    import torch
+
+    spec = sft.make_transform_spec("MDS5P6", 512.0, 10.0, sft.TransformOptions(precision=0))
+    n, batch, calls = 40000, 2, 7
+    plan = sft.TransformPlan(spec, n, batch=batch, mode=mode)
+    xs = [torch.from_numpy(np.stack([O.make_test_signal(O.SEEDED_NOISE, n, 100 + 3 * i + b) for b in range(batch)])
+                           .astype(np.float32)).pin_memory() for i in range(calls)]
+    outs = [torch.empty(tuple(plan.empty_output().shape), dtype=torch.float32).pin_memory() for _ in range(calls)]
+    for i in range(calls):
+        plan.execute_host_async(xs[i].numpy(), outs[i].numpy())
+    torch.cuda.current_stream().synchronize()
+    plan.synchronize()
+    ref = np.empty(tuple(outs[0].shape), dtype=np.float32)
+    for i in range(calls):
+        plan.execute_host(xs[i].numpy(), ref)
+        assert np.array_equal(outs[i].numpy(), ref)
