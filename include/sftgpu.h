@@ -252,8 +252,10 @@ int sftgpu_transform_execute_host_async(sftgpu_plan* plan, const void* x_host, v
 int sftgpu_plan_synchronize(sftgpu_plan* plan);
 /* 1 if the transform output is complex, 0 if real. */
 int sftgpu_plan_output_is_complex(const sftgpu_plan* plan);
-/* Plan geometry: info[0..7] = {sequential, direct-convolution, positions per thread,
- * positions per tile, warm-up tiles, chunks per signal, CTAs per launch, launches}. */
+/* Plan geometry: info[0..9] = {sequential, direct-convolution, positions per thread,
+ * positions per tile, warm-up tiles, chunks per signal, CTAs per launch, launches,
+ * orders evaluated, injection group mode of the first launch (0 shared real, 1 split,
+ * 2 per order, 3 shared complex)}. */
 int sftgpu_plan_describe(const sftgpu_plan* plan, int64_t* info, int n_info);
 /* Number of kernel launches one execute issues. */
 int sftgpu_plan_launches_per_execute(const sftgpu_plan* plan);

@@ -20,6 +20,9 @@ constexpr int lanes_per_thread() {
 // Group mode 1 (split injection) is instantiated for the multiplication method's layout:
 // NORD = 3P+2 orders of which the first P+1 (kappa terms) use the real constant.
 constexpr int split_na(int nord) { return (nord % 3 == 2) ? (nord + 1) / 3 : -1; }
+// Group mode 3 (one complex injection constant) is instantiated for 2P+1 orders: the
+// multiplication method once its kappa terms are below fp64 resolution (ξ ≳ 9).
+constexpr bool has_shared_complex(int nord) { return nord % 2 == 1; }
 
 struct LaunchKey {
   int nord, gm, mode, seq;
@@ -33,13 +36,17 @@ template <typename T, int NORD, int GM, int MODE, bool SEQ>
 static void launch_fixed(const ScanParams<T>& p, long long grid, cudaStream_t s) {
   constexpr int L = lanes_per_thread<T, SEQ>();
   constexpr int NA = GM == kGroupShared ? NORD : (GM == kGroupSplit ? split_na(NORD) : 0);
-  sft_scan_kernel<T, NORD, NA, GM, MODE, L, kThreads, SEQ><<<grid, kThreads, 0, s>>>(p);
+  constexpr int KGM = GM == kGroupSharedC ? kGroupSplit : GM;
+  sft_scan_kernel<T, NORD, NA, KGM, MODE, L, kThreads, SEQ><<<grid, kThreads, 0, s>>>(p);
 }
 
 template <typename T, int NORD, int MODE, bool SEQ>
 static void launch_gm(int gm, const ScanParams<T>& p, long long grid, cudaStream_t s) {
   if constexpr (MODE == kModeComplex && split_na(NORD) > 0) {
     if (gm == kGroupSplit) return launch_fixed<T, NORD, kGroupSplit, MODE, SEQ>(p, grid, s);
+  }
+  if constexpr (MODE == kModeComplex && has_shared_complex(NORD)) {
+    if (gm == kGroupSharedC) return launch_fixed<T, NORD, kGroupSharedC, MODE, SEQ>(p, grid, s);
   }
   if (gm == kGroupShared) return launch_fixed<T, NORD, kGroupShared, MODE, SEQ>(p, grid, s);
   launch_fixed<T, NORD, kGroupPerOrder, MODE, SEQ>(p, grid, s);

@@ -45,7 +45,10 @@ constexpr int kMaxL = 8;
 constexpr int kTabStride = 64;  // table entries per order (see layout below)
 
 enum Mode { kModeReal = 0, kModeComplex = 1, kModeComps = 2 };
-enum GroupMode { kGroupShared = 0, kGroupSplit = 1, kGroupPerOrder = 2 };
+// Injection group modes: 0 one real constant for all orders, 1 split (first NA orders
+// real constant, the rest one complex constant), 2 per order, 3 one complex constant
+// for all orders (host-side name; the kernel runs it as split with NA = 0).
+enum GroupMode { kGroupShared = 0, kGroupSplit = 1, kGroupPerOrder = 2, kGroupSharedC = 3 };
 
 template <typename T>
 struct Vec2;
@@ -279,34 +282,47 @@ __device__ __forceinline__ void window_carry(const ScanParams<T>& P, Smem<T, NOR
   __syncwarp();
 }
 
-// Loads the L lead / trail samples this thread stages for the tile starting at output
-// index o0 (coalesced, element e = tid + k*NT) into registers (prefetch). Interior
-// tiles (both windows inside the signal and past the warm start) skip all checks.
-template <typename T, int L, int NT>
-__device__ __forceinline__ void fetch_tile(const ScanParams<T>& P, const T* __restrict__ xs, long long lo,
-                                           long long o0, int tid, T (&fl)[L], T (&ft)[L]) {
+// Loads this thread's L samples (element e = tid + k*NT, coalesced) of one staged
+// stream starting at signal index j0. Samples before jmin are the virtual zeros ahead of
+// the warm start; indices outside [0, n) follow the boundary policy. A stream segment
+// lies inside the signal (fast path), entirely in one boundary region (uniform fill), or
+// straddles an edge (per-element checks: at most two segments per signal and stream).
+template <typename T, int L, int NT, bool KEEP>
+__device__ __forceinline__ void fetch_stream(const ScanParams<T>& P, const T* __restrict__ xs, long long j0,
+                                             long long jmin, int tid, unsigned long long pol, T (&f)[L]) {
   constexpr int TT = NT * L;
-  const long long lead_min = lo - P.K;  // virtual zero before the warm start
-  const unsigned long long pol = l2_keep_policy();
-  const long long l0 = lo + o0 + P.K, t0 = lo + o0 - P.K;
-  if (o0 >= 0 && t0 >= 0 && l0 + TT <= P.n && l0 >= lead_min) {
-    const T* pl = xs + l0 + tid;
-    const T* pt = xs + t0 + tid;
+  const long long n = P.n;
+  if (j0 >= jmin && j0 >= 0 && j0 + TT <= n) {
+    const T* p = xs + j0 + tid;
 #pragma unroll
-    for (int k = 0; k < L; ++k) {
-      fl[k] = ld_keep(pl + k * NT, pol);
-      ft[k] = __ldcs(pt + k * NT);
-    }
+    for (int k = 0; k < L; ++k) f[k] = KEEP ? ld_keep(p + k * NT, pol) : __ldcs(p + k * NT);
+    return;
+  }
+  if (j0 + TT <= jmin || (j0 >= jmin && (j0 >= n || j0 + TT <= 0))) {
+    T v = T(0);
+    if (j0 + TT > jmin && P.boundary != 0) v = __ldg(xs + (j0 >= n ? n - 1 : 0));
+#pragma unroll
+    for (int k = 0; k < L; ++k) f[k] = v;
     return;
   }
 #pragma unroll
   for (int k = 0; k < L; ++k) {
-    const long long o = o0 + tid + k * NT;
-    const long long pos = lo + o;
-    const long long jl = pos + P.K;
-    fl[k] = (jl >= lead_min) ? load_ext_keep(xs, P.n, P.boundary, jl, pol) : T(0);
-    ft[k] = (o >= 0) ? load_ext(xs, P.n, P.boundary, pos - P.K) : T(0);
+    const long long j = j0 + tid + k * NT;
+    f[k] = j < jmin ? T(0) : (KEEP ? load_ext_keep(xs, n, P.boundary, j, pol) : load_ext(xs, n, P.boundary, j));
   }
+}
+
+// Loads the L lead / trail samples this thread stages for the tile starting at output
+// index o0 into registers (prefetch). Output o reads lead x[lo+o+K] and trail
+// x[lo+o-K]; both are zero before the warm start (o < -2K for the lead, o < 0 for the
+// trail), i.e. below signal index lo - K in either stream.
+template <typename T, int L, int NT>
+__device__ __forceinline__ void fetch_tile(const ScanParams<T>& P, const T* __restrict__ xs, long long lo,
+                                           long long o0, int tid, T (&fl)[L], T (&ft)[L]) {
+  const long long jmin = lo - P.K;
+  const unsigned long long pol = l2_keep_policy();
+  fetch_stream<T, L, NT, true>(P, xs, lo + o0 + P.K, jmin, tid, pol, fl);
+  fetch_stream<T, L, NT, false>(P, xs, lo + o0 - P.K, jmin, tid, pol, ft);
 }
 
 // Complex arithmetic on the recurrence state. fp32: packed pair {re, im} in one 64-bit

@@ -347,7 +347,9 @@ void build_groups(sftgpu_plan* pl, std::vector<Order> ords, double alpha, double
     int na = 0;
     // components keep their order (outputs are per order); transforms may regroup
     g.gm = comps ? sftk::kGroupPerOrder : detect_groups(sub, alpha, pl->K, &cA, &cB, &na);
-    if (g.gm == sftk::kGroupSplit && (pl->mode != sftk::kModeComplex || sftk::split_na(g.nord) != na))
+    if (g.gm == sftk::kGroupSplit && na == 0 && pl->mode == sftk::kModeComplex && sftk::has_shared_complex(g.nord))
+      g.gm = sftk::kGroupSharedC;  // one complex constant for every order
+    else if (g.gm == sftk::kGroupSplit && (pl->mode != sftk::kModeComplex || sftk::split_na(g.nord) != na))
       g.gm = sftk::kGroupPerOrder;  // only the multiplication-method layout has a split kernel
     if (comps) {
       std::vector<Order> probe = sub;
@@ -366,8 +368,9 @@ void build_groups(sftgpu_plan* pl, std::vector<Order> ords, double alpha, double
     P.na = na;
     double Dr = 0, Di = 0;
     fill_consts<T>(P, sub, alpha, pref, pl->K, pl->L, comps, &Dr, &Di);
-    P.Dr = g0 == 0 ? static_cast<T>(Dr) : T(0);
-    P.Di = g0 == 0 ? static_cast<T>(Di) : T(0);
+    // each launch adds its own orders' share of the x[n-K] term
+    P.Dr = static_cast<T>(Dr);
+    P.Di = static_cast<T>(Di);
     build_tables<T>(g, sub, alpha, pl->L, pl->NT);
     P.tab = static_cast<const T*>(g.d_tab);
     P.tab_tile = g.d_tab_tile;
@@ -496,6 +499,17 @@ Lowered lower_spec(const sftb::Spec& s) {
     }
     default: fail(SFTGPU_EINVAL, "lower_spec: not an SFT transform kind");
   }
+  // Orders whose combine weights are below fp64 resolution of the largest weight add
+  // nothing representable to the output, in either precision: the reference still
+  // sums them (its result is unchanged by them), the kernel skips them. This is the
+  // multiplication method's kappa correction once e^{-xi^2/2} < 2^-63 (xi >= 9.4).
+  double wmax = 0.0;
+  for (const Order& o : lw.orders) wmax = std::max({wmax, std::abs(o.wc), std::abs(o.ws)});
+  const double floor_w = std::ldexp(wmax, -63);
+  std::vector<Order> kept;
+  for (const Order& o : lw.orders)
+    if (std::max(std::abs(o.wc), std::abs(o.ws)) > floor_w) kept.push_back(o);
+  if (!kept.empty()) lw.orders.swap(kept);
   return lw;
 }
 
@@ -1114,9 +1128,12 @@ int sftgpu_plan_output_is_complex(const sftgpu_plan* pl) { return pl && pl->mode
 int sftgpu_plan_describe(const sftgpu_plan* pl, int64_t* info, int n_info) {
   return guarded([&] {
     if (!pl || !info) fail(SFTGPU_EINVAL, "null argument");
-    const int64_t v[8] = {pl->seq, pl->conv, pl->L * 1LL, pl->TT, pl->warm_tiles, pl->n_chunks, pl->total_tiles,
-                          static_cast<int64_t>(pl->groups.size())};
-    for (int i = 0; i < n_info && i < 8; ++i) info[i] = v[i];
+    int64_t orders = 0;
+    for (const Group& g : pl->groups) orders += g.nord;
+    const int64_t v[10] = {pl->seq, pl->conv, pl->L * 1LL, pl->TT, pl->warm_tiles, pl->n_chunks, pl->total_tiles,
+                           static_cast<int64_t>(pl->groups.size()), orders,
+                           pl->groups.empty() ? -1 : pl->groups[0].gm};
+    for (int i = 0; i < n_info && i < 10; ++i) info[i] = v[i];
   });
 }
 

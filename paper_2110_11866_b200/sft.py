@@ -579,11 +579,16 @@ class TransformPlan:
         self.launches = lib().sftgpu_plan_launches_per_execute(h)
 
     def describe(self) -> dict:
-        info = (C.c_int64 * 8)()
-        check(lib().sftgpu_plan_describe(self._h, info, 8))
+        info = (C.c_int64 * 10)()
+        check(lib().sftgpu_plan_describe(self._h, info, 10))
         keys = ("sequential", "direct_convolution", "positions_per_thread", "positions_per_tile", "warm_tiles",
-                "chunks_per_signal", "ctas_per_launch", "launches")
+                "chunks_per_signal", "ctas_per_launch", "launches", "orders", "group_mode")
         return dict(zip(keys, list(info)))
+
+    @property
+    def orders(self) -> int:
+        """Basis orders the kernels evaluate (after dropping below-resolution terms)."""
+        return self.describe()["orders"]
 
     def dtype(self):
         torch = _torch()

@@ -418,12 +418,12 @@ def test_chunked_sequential_matches_lookback(sft, O, abbrev, sigma, xi, prec, to
 @pytest.mark.parametrize("prec,tol", [(0, 1e-5), (1, 1e-12)])
 @pytest.mark.parametrize("boundary", [0, 1])
 def test_split_launches_modes_boundaries(sft, O, mode, prec, tol, boundary):
-    """17 orders (MMS5P5: 11 real-frequency + 6 kappa orders) run as two accumulating
-    launches; both execution modes, both precisions and both boundary policies agree
-    with the oracle."""
+    """17 orders (MMS5P5: 11 real-frequency + 6 kappa orders; xi=6 keeps the kappa terms
+    above fp64 resolution) run as two accumulating launches; both execution modes, both
+    precisions and both boundary policies agree with the oracle."""
     import torch
 
-    spec = sft.make_transform_spec("MMS5P5", 60.0, 10.0, sft.TransformOptions(precision=prec))
+    spec = sft.make_transform_spec("MMS5P5", 60.0, 6.0, sft.TransformOptions(precision=prec))
     n = 20011
     x = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 3, 2, sft.Precision(prec))
     plan = sft.TransformPlan(spec, n, 2, boundary, mode=mode)
@@ -503,3 +503,25 @@ def test_pipelined_host_execution(sft, O, mode):
     for i in range(calls):
         plan.execute_host(xs[i].numpy(), ref)
         assert np.array_equal(outs[i].numpy(), ref)
+
+
+@pytest.mark.parametrize("xi,nord", [(10.0, 7), (6.0, 11)])
+def test_multiply_kappa_terms_below_resolution_are_skipped(sft, O, xi, nord):
+    """The multiplication method's kappa correction (transforms.cpp:373-428) scales with
+    e^{-xi^2/2}: at xi=10 it is ~2e-22 of the envelope weights, below fp64 resolution,
+    and the plan drops those orders (one complex injection constant for the remaining
+    2P+1); at xi=6 they stay. Either way the result matches the oracle, which sums all
+    3P+2 orders."""
+    import torch
+
+    spec = sft.make_transform_spec("MMS5P3", 300.0, xi, sft.TransformOptions(precision=1))
+    n = 9001
+    plan = sft.TransformPlan(spec, n, 1, mode="lookback")
+    x = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 5, 1, sft.Precision.Double)
+    out = plan.empty_output()
+    plan.execute(x, out)
+    torch.cuda.synchronize()
+    assert plan.orders == nord
+    ref = oracle_transform(O, x[0].cpu().numpy(), 1, spec)
+    oh = out[0].cpu().numpy()
+    assert rel_max(oh[:, 0] + 1j * oh[:, 1], ref) < 1e-12
