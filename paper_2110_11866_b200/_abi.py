@@ -10,6 +10,8 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libsftgpu.so")
+# A/B experiments may point the package at another build of the same ABI.
+LIB_PATH = os.environ.get("SFTGPU_LIB", LIB_PATH)
 
 MAX_COEFFS = 64
 

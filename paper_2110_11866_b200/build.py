@@ -46,8 +46,21 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
+def _flags_stamp() -> None:
+    """Invalidate cached objects when the compile flags change."""
+    stamp = os.path.join(BUILD, "flags.txt")
+    flags = " ".join(ARCH + COMMON)
+    old = open(stamp).read() if os.path.exists(stamp) else None
+    if old != flags:
+        for o in glob.glob(os.path.join(BUILD, "*.o")):
+            os.remove(o)
+        with open(stamp, "w") as f:
+            f.write(flags)
+
+
 def build(verbose: bool = False, jobs: int | None = None) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    _flags_stamp()
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     with ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))

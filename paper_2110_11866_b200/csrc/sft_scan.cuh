@@ -38,7 +38,7 @@
 namespace sftk {
 
 #ifndef SFTK_SEQ_MINB
-#define SFTK_SEQ_MINB 4
+#define SFTK_SEQ_MINB 8
 #endif
 constexpr int kMaxOrd = 12;
 constexpr int kMaxL = 8;
@@ -159,13 +159,6 @@ __device__ __forceinline__ T load_ext(const T* __restrict__ xs, long long n, int
   return __ldg(xs + (j < 0 ? 0 : n - 1));
 }
 
-template <typename T>
-__device__ __forceinline__ T load_ext_keep(const T* __restrict__ xs, long long n, int bnd, long long j,
-                                           unsigned long long pol) {
-  if (j >= 0 && j < n) return ld_keep(xs + j, pol);
-  if (bnd == 0) return T(0);
-  return __ldg(xs + (j < 0 ? 0 : n - 1));
-}
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -282,11 +275,62 @@ __device__ __forceinline__ void window_carry(const ScanParams<T>& P, Smem<T, NOR
   __syncwarp();
 }
 
-// Loads this thread's L samples (element e = tid + k*NT, coalesced) of one staged
-// stream starting at signal index j0. Samples before jmin are the virtual zeros ahead of
-// the warm start; indices outside [0, n) follow the boundary policy. A stream segment
-// lies inside the signal (fast path), entirely in one boundary region (uniform fill), or
-// straddles an edge (per-element checks: at most two segments per signal and stream).
+// ---- asynchronous staging (LDGSTS): global -> shared without holding registers
+__device__ __forceinline__ unsigned long long l2_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+template <typename T>
+__device__ __forceinline__ void cp_async(T* dst, const T* src, unsigned long long pol) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], %2, %3;"
+               :: "r"(d), "l"(src), "n"(sizeof(T)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Stages one stream of a tile (element e = tid + k*NT, coalesced) starting at signal
+// index j0 into shared memory (padded index e + e/32). Samples before jmin are the
+// virtual zeros ahead of the warm start; indices outside [0, n) follow the boundary
+// policy. A segment lies inside the signal (asynchronous copies), entirely in one
+// boundary region (uniform fill), or straddles an edge (per-element checks: at most
+// two segments per signal and stream).
+template <typename T, int L, int NT>
+__device__ __forceinline__ void stage_stream(const ScanParams<T>& P, const T* __restrict__ xs, long long j0,
+                                             long long jmin, int tid, unsigned long long pol, T* dst) {
+  constexpr int TT = NT * L;
+  const long long n = P.n;
+  if (j0 >= jmin && j0 >= 0 && j0 + TT <= n) {
+    const T* src = xs + j0;
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      const int e = tid + k * NT;
+      cp_async(dst + e + (e >> 5), src + e, pol);
+    }
+    return;
+  }
+  if (j0 + TT <= jmin || (j0 >= jmin && (j0 >= n || j0 + TT <= 0))) {
+    T v = T(0);
+    if (j0 + TT > jmin && P.boundary != 0) v = __ldg(xs + (j0 >= n ? n - 1 : 0));
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      const int e = tid + k * NT;
+      dst[e + (e >> 5)] = v;
+    }
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < L; ++k) {
+    const int e = tid + k * NT;
+    const long long j = j0 + e;
+    dst[e + (e >> 5)] = j < jmin ? T(0) : load_ext(xs, n, P.boundary, j);
+  }
+}
+
+// Register variant of stage_stream (same classification), for the one-tile LB path:
+// both streams' loads are issued before any shared-memory store, so the two DRAM
+// round trips overlap.
 template <typename T, int L, int NT, bool KEEP>
 __device__ __forceinline__ void fetch_stream(const ScanParams<T>& P, const T* __restrict__ xs, long long j0,
                                              long long jmin, int tid, unsigned long long pol, T (&f)[L]) {
@@ -308,21 +352,34 @@ __device__ __forceinline__ void fetch_stream(const ScanParams<T>& P, const T* __
 #pragma unroll
   for (int k = 0; k < L; ++k) {
     const long long j = j0 + tid + k * NT;
-    f[k] = j < jmin ? T(0) : (KEEP ? load_ext_keep(xs, n, P.boundary, j, pol) : load_ext(xs, n, P.boundary, j));
+    f[k] = j < jmin ? T(0) : load_ext(xs, n, P.boundary, j);
   }
 }
 
-// Loads the L lead / trail samples this thread stages for the tile starting at output
-// index o0 into registers (prefetch). Output o reads lead x[lo+o+K] and trail
+// Stages the tile starting at output index o0: output o reads lead x[lo+o+K] and trail
 // x[lo+o-K]; both are zero before the warm start (o < -2K for the lead, o < 0 for the
-// trail), i.e. below signal index lo - K in either stream.
-template <typename T, int L, int NT>
-__device__ __forceinline__ void fetch_tile(const ScanParams<T>& P, const T* __restrict__ xs, long long lo,
-                                           long long o0, int tid, T (&fl)[L], T (&ft)[L]) {
+// trail), i.e. below signal index lo - K in either stream. Leading samples are re-read
+// 2K positions later as trailing samples (L2 evict_last); trailing reads are their last
+// use (evict_first). Completion: cp_async_wait_all + barrier.
+template <typename T, int L, int NT, bool ASYNC>
+__device__ __forceinline__ void stage_tile(const ScanParams<T>& P, const T* __restrict__ xs, long long lo,
+                                           long long o0, int tid, T* sl, T* stl) {
   const long long jmin = lo - P.K;
-  const unsigned long long pol = l2_keep_policy();
-  fetch_stream<T, L, NT, true>(P, xs, lo + o0 + P.K, jmin, tid, pol, fl);
-  fetch_stream<T, L, NT, false>(P, xs, lo + o0 - P.K, jmin, tid, pol, ft);
+  if constexpr (ASYNC) {
+    stage_stream<T, L, NT>(P, xs, lo + o0 + P.K, jmin, tid, l2_keep_policy(), sl);
+    stage_stream<T, L, NT>(P, xs, lo + o0 - P.K, jmin, tid, l2_first_policy(), stl);
+    cp_async_commit();
+  } else {
+    T fl[L], ft[L];
+    fetch_stream<T, L, NT, true>(P, xs, lo + o0 + P.K, jmin, tid, l2_keep_policy(), fl);
+    fetch_stream<T, L, NT, false>(P, xs, lo + o0 - P.K, jmin, tid, 0ull, ft);
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      const int e = tid + k * NT;
+      sl[e + (e >> 5)] = fl[k];
+      stl[e + (e >> 5)] = ft[k];
+    }
+  }
 }
 
 // Complex arithmetic on the recurrence state. fp32: packed pair {re, im} in one 64-bit
@@ -411,8 +468,8 @@ struct Cx<double> {
 template <typename T, int NORD, int NA, int GM, int MODE, int L, int NT, bool SEQ>
 __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L, NT, SEQ>& S, long long sig,
                                         long long gt, long long first, long long lo, long long count,
-                                        long long obase, long long o0, T (&fl)[L], T (&ft)[L],
-                                        const T* __restrict__ xs, bool has_next) {
+                                        long long obase, long long o0, const T* __restrict__ xs,
+                                        bool has_next) {
   using X = Cx<T>;
   using St = typename X::S;
   using T2 = typename Vec2<T>::t;
@@ -426,14 +483,11 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
   T* const sl = S.lead[b];
   T* const stl = S.trail[b];
 
-#pragma unroll
-  for (int k = 0; k < L; ++k) {
-    const int e = tid + k * NT;
-    sl[e + (e >> 5)] = fl[k];
-    stl[e + (e >> 5)] = ft[k];
+  if constexpr (SEQ) cp_async_wait_all();
+  __syncthreads();  // this tile staged; the other buffer's last readers are done
+  if constexpr (SEQ) {
+    if (has_next) stage_tile<T, L, NT, true>(P, xs, lo, o0 + TT, tid, S.lead[b ^ 1], S.trail[b ^ 1]);
   }
-  __syncthreads();
-  if (has_next) fetch_tile<T, L, NT>(P, xs, lo, o0 + TT, tid, fl, ft);  // in flight during this tile
 
   if constexpr (!SEQ) {
     // ---- lead-only aggregates (whole tile and its last r positions), published for
@@ -483,44 +537,37 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
     if (warm) return;  // warm tiles only feed their successors' windows
   }
 
-  // ---- injections, shared across orders where the group mode allows
-  T xt_[L];
-  St gA[L];  // {x[n+K] - cA x[n-K], 0}
-  constexpr int LB = GM == kGroupSplit ? L : 1;
-  St gB[LB];  // {x[n+K] - Re(cB) x[n-K], -Im(cB) x[n-K]}
-#pragma unroll
-  for (int i = 0; i < L; ++i) {
+  // ---- injections, shared across orders where the group mode allows. Samples are
+  // read from shared memory per position in both phases (no per-position registers).
+  // gA = x[n+K] - cA x[n-K] (real), gB = x[n+K] - cB x[n-K] (complex, split modes).
+  auto sample = [&](int i, T& xl, T& xt) {
     const int e = tid * L + i;
-    const T xl = sl[e + (e >> 5)], xt = stl[e + (e >> 5)];
-    xt_[i] = xt;
-    gA[i] = X::make(GM == kGroupPerOrder ? xl : fma(-P.cAr, xt, xl), T(0));
-    if constexpr (GM == kGroupSplit) gB[i] = X::make(fma(-P.cBr, xt, xl), -P.cBi * xt);
-  }
-  // Per-order injection (group mode 2) is recomputed in phase 2 from shared memory;
-  // the volatile re-read keeps the compiler from caching NORD*L complex values.
-  auto inj = [&](const OrdConst<T>& c, int p, int i, bool reload) -> St {
-    if (GM == kGroupShared || (GM == kGroupSplit && p < NA)) return gA[i];
-    if constexpr (GM == kGroupSplit) return gB[i];
-    const int e = tid * L + i;
-    const T xl = reload ? *reinterpret_cast<volatile const T*>(sl + e + (e >> 5)) : sl[e + (e >> 5)];
-    const T xt = reload ? *reinterpret_cast<volatile const T*>(stl + e + (e >> 5)) : xt_[i];
+    xl = sl[e + (e >> 5)];
+    xt = stl[e + (e >> 5)];
+  };
+  auto inj = [&](const OrdConst<T>& c, int p, T xl, T xt) -> St {
+    if (GM == kGroupShared || (GM == kGroupSplit && p < NA)) return X::make(fma(-P.cAr, xt, xl), T(0));
+    if constexpr (GM == kGroupSplit) return X::make(fma(-P.cBr, xt, xl), -P.cBi * xt);
     return X::make(fma(-c.cc[0], xt, xl), -c.cc[1] * xt);
   };
 
-  // ---- phase 1: per-thread aggregate with zero state in
+  // ---- phase 1: per-thread aggregate with zero state in (positions outer; each
+  // order's sum runs over i in the same order as a per-order loop would)
   St st[NORD];
 #pragma unroll
-  for (int p = 0; p < NORD; ++p) {
-    const OrdConst<T>& c = P.oc[p];
-    St acc = X::zero();
-    if (GM == kGroupShared || (GM == kGroupSplit && p < NA)) {
+  for (int p = 0; p < NORD; ++p) st[p] = X::zero();
 #pragma unroll
-      for (int i = 0; i < L; ++i) acc = X::agg_r(c, i, X::re(gA[i]), acc);
-    } else {
+  for (int i = 0; i < L; ++i) {
+    T xl, xt;
+    sample(i, xl, xt);
 #pragma unroll
-      for (int i = 0; i < L; ++i) acc = X::agg_c(c, i, inj(c, p, i, false), acc);
+    for (int p = 0; p < NORD; ++p) {
+      const OrdConst<T>& c = P.oc[p];
+      if (GM == kGroupShared || (GM == kGroupSplit && p < NA))
+        st[p] = X::agg_r(c, i, fma(-P.cAr, xt, xl), st[p]);
+      else
+        st[p] = X::agg_c(c, i, inj(c, p, xl, xt), st[p]);
     }
-    st[p] = acc;
   }
 
   // ---- warp-level exclusive scan, transposed: every thread parks its per-order
@@ -616,11 +663,13 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
       T* sptr = P.out_s + p * P.ord_stride + sig * P.ld_out + obase;
 #pragma unroll
       for (int i = 0; i < L; ++i) {
-        v = X::step(c, v, inj(c, p, i, true));
+        T xl, xt;
+        sample(i, xl, xt);
+        v = X::step(c, v, inj(c, p, xl, xt));
         const long long o = ob + i;
         if (o < count) {
           // c = Re(a V + b x_t), s = -Im(a V + b x_t), a = (k1, k2), b = (k3, k4) = (ka[1], kb[1])
-          const T vr = X::re(v), vi = X::im(v), xt = xt_[i];
+          const T vr = X::re(v), vi = X::im(v);
           cptr[o] = fma(c.ka[0], vr, fma(-c.kb[0], vi, c.ka[1] * xt));
           sptr[o] = -fma(c.kb[0], vr, fma(c.ka[0], vi, c.kb[1] * xt));
         }
@@ -628,54 +677,61 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
     }
   } else {
     constexpr bool CPLX = MODE == kModeComplex;
-    constexpr int CW = CPLX ? 2 : 1;  // T words per output
-    T buf[L * CW];
-    // positions outer, orders inner: NORD independent recurrence chains per position
-    // (same per-output accumulation order as orders-outer, so results are identical)
-#pragma unroll
-    for (int i = 0; i < L; ++i) {
-      St acc = X::make(P.Dr * xt_[i], CPLX ? P.Di * xt_[i] : T(0));
-      T accr = P.Dr * xt_[i];
-#pragma unroll
-      for (int p = 0; p < NORD; ++p) {
-        const OrdConst<T>& c = P.oc[p];
-        st[p] = X::step(c, st[p], inj(c, p, i, true));
-        if constexpr (CPLX)
-          acc = X::comb(c, st[p], acc);
-        else
-          accr = X::comb_re(c, st[p], accr);
-      }
-      if constexpr (CPLX) {
-        buf[2 * i] = X::re(acc);
-        buf[2 * i + 1] = X::im(acc);
-      } else {
-        buf[i] = accr;
-      }
-    }
-    // ---- stores: L consecutive outputs per thread, 16-byte vectors when aligned
-    T* optr = P.out + CW * (sig * P.ld_out + obase);
+    constexpr int CW = CPLX ? 2 : 1;    // T words per output
     constexpr int VW = 16 / sizeof(T);  // T words per 16-byte vector
-    if (P.vec_ok && !P.accumulate && ob + L <= count && (L * CW) % VW == 0) {
-      T* dst = optr + ob * CW;
+    constexpr int VP = VW / CW;         // outputs per vector
+    static_assert(L % VP == 0, "positions per thread must fill whole vectors");
+    constexpr int CH = VP;  // outputs computed per store batch
+    T* const optr = P.out + CW * (sig * P.ld_out + obase);
+    const bool vec = P.vec_ok && !P.accumulate && ob + L <= count;
+    // positions outer, orders inner: NORD independent recurrence chains per position
 #pragma unroll
-      for (int v = 0; v < L * CW / VW; ++v) {
-        if constexpr (sizeof(T) == 4)
-          __stcs(reinterpret_cast<float4*>(dst) + v,
-                 make_float4(buf[v * 4], buf[v * 4 + 1], buf[v * 4 + 2], buf[v * 4 + 3]));
-        else
-          __stcs(reinterpret_cast<double2*>(dst) + v, make_double2(buf[v * 2], buf[v * 2 + 1]));
+    for (int i0 = 0; i0 < L; i0 += CH) {
+      T buf[CH * CW];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        T xl, xt;
+        sample(i0 + j, xl, xt);
+        St acc = X::make(P.Dr * xt, CPLX ? P.Di * xt : T(0));
+        T accr = P.Dr * xt;
+#pragma unroll
+        for (int p = 0; p < NORD; ++p) {
+          const OrdConst<T>& c = P.oc[p];
+          st[p] = X::step(c, st[p], inj(c, p, xl, xt));
+          if constexpr (CPLX)
+            acc = X::comb(c, st[p], acc);
+          else
+            accr = X::comb_re(c, st[p], accr);
+        }
+        if constexpr (CPLX) {
+          buf[2 * j] = X::re(acc);
+          buf[2 * j + 1] = X::im(acc);
+        } else {
+          buf[j] = accr;
+        }
       }
-    } else {
+      if (vec) {
+        T* dst = optr + (ob + i0) * CW;
 #pragma unroll
-      for (int i = 0; i < L; ++i) {
-        const long long o = ob + i;
-        if (o < count) {
+        for (int v = 0; v < CH * CW / VW; ++v) {
+          if constexpr (sizeof(T) == 4)
+            __stcs(reinterpret_cast<float4*>(dst) + v,
+                   make_float4(buf[4 * v], buf[4 * v + 1], buf[4 * v + 2], buf[4 * v + 3]));
+          else
+            __stcs(reinterpret_cast<double2*>(dst) + v, make_double2(buf[2 * v], buf[2 * v + 1]));
+        }
+      } else {
 #pragma unroll
-          for (int w = 0; w < CW; ++w) {
-            if (P.accumulate)
-              optr[o * CW + w] += buf[i * CW + w];
-            else
-              optr[o * CW + w] = buf[i * CW + w];
+        for (int j = 0; j < CH; ++j) {
+          const long long o = ob + i0 + j;
+          if (o < count) {
+#pragma unroll
+            for (int w = 0; w < CW; ++w) {
+              if (P.accumulate)
+                optr[o * CW + w] += buf[j * CW + w];
+              else
+                optr[o * CW + w] = buf[j * CW + w];
+            }
           }
         }
       }
@@ -684,13 +740,12 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
 }
 
 template <typename T, int NORD, int NA, int GM, int MODE, int L, int NT, bool SEQ>
-__global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? SFTK_SEQ_MINB : 4) : 2)) sft_scan_kernel(const __grid_constant__ ScanParams<T> P) {
+__global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? (NORD <= 8 ? SFTK_SEQ_MINB : 6) : 4) : 2)) sft_scan_kernel(const __grid_constant__ ScanParams<T> P) {
   static_assert(NORD >= 1 && NORD <= kMaxOrd, "order count");
   static_assert(L <= kMaxL, "positions per thread");
   constexpr int TT = NT * L;
   __shared__ Smem<T, NORD, L, NT, SEQ> S;
   const int tid = threadIdx.x;
-  T fl[L], ft[L];
 
   if constexpr (SEQ) {
     // one CTA per (signal, chunk): tiles in order from the chunk's own warm start,
@@ -704,9 +759,10 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? SFTK_SEQ_MINB : 4
     const T* __restrict__ xs = P.x + sig * P.ld_x;
     if (tid < NORD) S.carry[tid] = make_double2(0.0, 0.0);
     const long long o_first = -P.warm_tiles * TT;
-    fetch_tile<T, L, NT>(P, xs, lo, o_first, tid, fl, ft);
+    const int b0 = static_cast<int>(((o_first / TT) % 2 + 2) % 2);
+    stage_tile<T, L, NT, true>(P, xs, lo, o_first, tid, S.lead[b0], S.trail[b0]);
     for (long long t = 0; t < tiles; ++t)
-      do_tile<T, NORD, NA, GM, MODE, L, NT, true>(P, S, sig, 0, 0, lo, count, obase, o_first + t * TT, fl, ft, xs,
+      do_tile<T, NORD, NA, GM, MODE, L, NT, true>(P, S, sig, 0, 0, lo, count, obase, o_first + t * TT, xs,
                                                   t + 1 < tiles);
   } else {
     if (tid == 0) {
@@ -726,8 +782,8 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? SFTK_SEQ_MINB : 4
     const long long first = sig * P.tiles_per_signal;
     const long long o0 = (gt - first - P.warm_tiles) * TT;
     const T* __restrict__ xs = P.x + sig * P.ld_x;
-    fetch_tile<T, L, NT>(P, xs, P.lo, o0, tid, fl, ft);
-    do_tile<T, NORD, NA, GM, MODE, L, NT, false>(P, S, sig, gt, first, P.lo, P.count, 0, o0, fl, ft, xs, false);
+    stage_tile<T, L, NT, false>(P, xs, P.lo, o0, tid, S.lead[0], S.trail[0]);
+    do_tile<T, NORD, NA, GM, MODE, L, NT, false>(P, S, sig, gt, first, P.lo, P.count, 0, o0, xs, false);
   }
 }
 
