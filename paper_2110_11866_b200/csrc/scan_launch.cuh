@@ -9,7 +9,7 @@ namespace sftk {
 // Tile geometry: NT threads x L positions. SEQ (batched) uses long tiles; LB (one
 // tile per CTA) uses shorter tiles so a single signal still spreads over the SMs.
 constexpr int kThreads = 128;
-constexpr int kLSeqF32 = 8, kLSeqF64 = 4;
+constexpr int kLSeqF32 = 16, kLSeqF64 = 4;
 constexpr int kLLbF32 = 8, kLLbF64 = 4;
 
 template <typename T, bool SEQ>
@@ -37,7 +37,16 @@ static void launch_fixed(const ScanParams<T>& p, long long grid, cudaStream_t s)
   constexpr int L = lanes_per_thread<T, SEQ>();
   constexpr int NA = GM == kGroupShared ? NORD : (GM == kGroupSplit ? split_na(NORD) : 0);
   constexpr int KGM = GM == kGroupSharedC ? kGroupSplit : GM;
-  sft_scan_kernel<T, NORD, NA, KGM, MODE, L, kThreads, SEQ><<<grid, kThreads, 0, s>>>(p);
+  constexpr size_t smem = sizeof(Smem<T, NORD, L, kThreads, SEQ>);
+  auto* kern = &sft_scan_kernel<T, NORD, NA, KGM, MODE, L, kThreads, SEQ>;
+  if constexpr (smem > 48 * 1024) {
+    // one process drives one GPU: the opt-in is made once per process
+    // (if it failed, the launch below fails and run_groups reports it)
+    static const cudaError_t opt_in =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    (void)opt_in;
+  }
+  kern<<<grid, kThreads, smem, s>>>(p);
 }
 
 template <typename T, int NORD, int MODE, bool SEQ>

@@ -41,7 +41,7 @@ namespace sftk {
 #define SFTK_SEQ_MINB 8
 #endif
 constexpr int kMaxOrd = 12;
-constexpr int kMaxL = 8;
+constexpr int kMaxL = 16;
 constexpr int kTabStride = 64;  // table entries per order (see layout below)
 
 enum Mode { kModeReal = 0, kModeComplex = 1, kModeComps = 2 };
@@ -227,8 +227,18 @@ struct Smem {
   double2 tsfx[NORD];     // LB: lead-only aggregate of the tile's last r positions
   T2 wla[NW][NORD];       // LB: per-warp lead-only totals
   T2 wsa[NW][NORD];       // LB: per-warp lead-only suffix totals
-  T2 wscan[NW][NORD * 33];          // per-warp transposed scan staging (padded)
-  double2 pay[SEQ ? 1 : 64][NORD];  // LB window-carry staging (64 predecessors per round)
+  // The transposed-scan staging is dead once the scan's barrier has passed; the LB
+  // window carry (warp 0, after that barrier) reuses it.
+  union {
+    T2 wscan[NW][NORD * 33];          // per-warp transposed scan staging (padded)
+    double2 pay[SEQ ? 1 : 64][NORD];  // LB window-carry staging (64 predecessors per round)
+  };
+  T2 wst[NW][NORD][4];              // per-warp segment starts of the transposed scan
+  // powers for folding segment starts into thread states ({re, re, -im, im} entries):
+  // [p][r] = z^{L r} (r < SEG), [p][SEG + g] = z^{L SEG g} (g < SEGS)
+  static constexpr int SEG = NORD <= 8 ? 8 : 16;
+  static constexpr int SEGS = 32 / SEG;
+  T ptab[NORD][SEG + SEGS][4];
   long long tile;
   unsigned int epoch;
 };
@@ -417,8 +427,8 @@ struct Cx<float> {
   static __device__ __forceinline__ S agg_c(const C& c, int i, S g, S acc) {
     return fma2(ldp(&c.w[i][2]), pk(im(g), im(g)), fma2(ldp(&c.w[i][0]), pk(re(g), re(g)), acc));
   }
-  static __device__ __forceinline__ S shfl_up(S v, int d) {
-    return pk(__shfl_up_sync(0xffffffffu, re(v), d), __shfl_up_sync(0xffffffffu, im(v), d));
+  static __device__ __forceinline__ S shfl(S v, int src) {
+    return pk(__shfl_sync(0xffffffffu, re(v), src), __shfl_sync(0xffffffffu, im(v), src));
   }
   static __device__ __forceinline__ S warp_sum(S v) {
 #pragma unroll
@@ -456,8 +466,8 @@ struct Cx<double> {
   static __device__ __forceinline__ S agg_c(const C& c, int i, S g, S acc) {
     return make_double2(fma(c.w[i][0], g.x, fma(-c.w[i][1], g.y, acc.x)), fma(c.w[i][1], g.x, fma(c.w[i][0], g.y, acc.y)));
   }
-  static __device__ __forceinline__ S shfl_up(S v, int d) {
-    return make_double2(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
+  static __device__ __forceinline__ S shfl(S v, int src) {
+    return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
   }
   static __device__ __forceinline__ S warp_sum(S v) { return warp_sum2(v); }
 };
@@ -570,24 +580,46 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
     }
   }
 
-  // ---- warp-level exclusive scan, transposed: every thread parks its per-order
-  // aggregates in shared memory, then lane p runs the 32-step Horner chain for order p
-  // (padded stride 33: conflict-free), writing each lane's exclusive prefix in place.
+  // ---- warp-level exclusive scan, transposed and segmented: every thread parks its
+  // per-order aggregates in shared memory (padded stride 33: conflict-free). The 32
+  // aggregates of an order are cut into SEGS segments of SEG; lane (segment g, order p)
+  // runs the SEG-step Horner chain of its segment, writing local exclusive prefixes in
+  // place, and the segment totals are chained across lanes with SEGS-1 shuffles. The
+  // segment start is folded into the per-thread state once the warp carry is known.
+  constexpr int SEG = Smem<T, NORD, L, NT, SEQ>::SEG;
+  constexpr int SEGS = Smem<T, NORD, L, NT, SEQ>::SEGS;
   {
     T2* wa = S.wscan[warp];
 #pragma unroll
     for (int p = 0; p < NORD; ++p) wa[p * 33 + lane] = make2<T2>(X::re(st[p]), X::im(st[p]));
     __syncwarp();
-    if (lane < NORD) {
-      const T* zl = P.oc[lane].scan[0];  // z^L
-      St run = X::zero();
-#pragma unroll 8
-      for (int j = 0; j < 32; ++j) {
-        const T2 a = wa[lane * 33 + j];
-        wa[lane * 33 + j] = make2<T2>(X::re(run), X::im(run));
+    const int sp = lane % SEG, sg = lane / SEG;
+    const bool act = sp < NORD;
+    const int po = act ? sp : 0;
+    St run = X::zero();
+    if (act) {
+      const T* zl = P.oc[sp].scan[0];  // z^L
+#pragma unroll
+      for (int j = 0; j < SEG; ++j) {
+        const int idx = sp * 33 + sg * SEG + j;
+        const T2 a = wa[idx];
+        wa[idx] = make2<T2>(X::re(run), X::im(run));
         run = X::madd(zl, run, X::make(a.x, a.y));
       }
-      S.w[warp][lane] = make2<T2>(X::re(run), X::im(run));
+    }
+    const T* zs = S.ptab[po][SEG + 1];  // z^{L SEG}
+    St start = X::zero();
+#pragma unroll
+    for (int g = 0; g < SEGS - 1; ++g) {
+      const St tg = X::shfl(run, sp + g * SEG);
+      if (g < sg) start = X::madd(zs, start, tg);
+    }
+    if (act) {
+      S.wst[warp][sp][sg] = make2<T2>(X::re(start), X::im(start));
+      if (sg == SEGS - 1) {
+        const St tot = X::madd(zs, start, run);
+        S.w[warp][sp] = make2<T2>(X::re(tot), X::im(tot));
+      }
     }
     __syncwarp();
 #pragma unroll
@@ -645,11 +677,18 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
   __syncthreads();
   if (warm) return;  // SEQ warm tile: phase 1 only (uniform per CTA)
 
-  // state entering this thread's segment: z^{L*lane} * Cw + in-warp exclusive
+  // state entering this thread's positions:
+  //   z^{L lane} Cw + exclusive(lane) = e_local + z^{L r} (start_g + z^{L SEG g} Cw),
+  // lane = g SEG + r, e_local its in-segment exclusive prefix
+  {
+    const int g = lane / SEG, r = lane % SEG;
 #pragma unroll
-  for (int p = 0; p < NORD; ++p) {
-    const T2 cw = S.w[warp][p];
-    st[p] = X::madd(P.tab + (p * kTabStride + lane) * 4, X::make(cw.x, cw.y), st[p]);
+    for (int p = 0; p < NORD; ++p) {
+      const T2 cw = S.w[warp][p];
+      const T2 s0 = S.wst[warp][p][g];
+      const St adj = X::madd(S.ptab[p][SEG + g], X::make(cw.x, cw.y), X::make(s0.x, s0.y));
+      st[p] = X::madd(S.ptab[p][r], adj, st[p]);
+    }
   }
 
   // ---- phase 2: re-run the recurrence from the true state and combine
@@ -740,12 +779,22 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
 }
 
 template <typename T, int NORD, int NA, int GM, int MODE, int L, int NT, bool SEQ>
-__global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? (NORD <= 8 ? SFTK_SEQ_MINB : 6) : 4) : 2)) sft_scan_kernel(const __grid_constant__ ScanParams<T> P) {
+__global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? (L >= 16 ? 5 : (NORD <= 8 ? SFTK_SEQ_MINB : 6)) : 4) : 2)) sft_scan_kernel(const __grid_constant__ ScanParams<T> P) {
   static_assert(NORD >= 1 && NORD <= kMaxOrd, "order count");
   static_assert(L <= kMaxL, "positions per thread");
   constexpr int TT = NT * L;
-  __shared__ Smem<T, NORD, L, NT, SEQ> S;
+  extern __shared__ __align__(16) unsigned char smem_raw[];  // sized by the launcher
+  Smem<T, NORD, L, NT, SEQ>& S = *reinterpret_cast<Smem<T, NORD, L, NT, SEQ>*>(smem_raw);
   const int tid = threadIdx.x;
+  {
+    using Sm = Smem<T, NORD, L, NT, SEQ>;
+    constexpr int E = Sm::SEG + Sm::SEGS;
+    for (int q = tid; q < NORD * E * 4; q += NT) {
+      const int p = q / (E * 4), j = (q / 4) % E, w = q % 4;
+      const int src = j < Sm::SEG ? j : Sm::SEG * (j - Sm::SEG);
+      S.ptab[p][j][w] = P.tab[(p * kTabStride + src) * 4 + w];
+    }
+  }
 
   if constexpr (SEQ) {
     // one CTA per (signal, chunk): tiles in order from the chunk's own warm start,
