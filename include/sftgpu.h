@@ -228,7 +228,10 @@ int sftgpu_transform_plan_create(const sftgpu_spec* spec, int64_t n, int64_t bat
 int sftgpu_transform_plan_create_range(const sftgpu_spec* spec, int64_t n, int64_t batch, int boundary,
                                        int64_t out_begin, int64_t out_count, sftgpu_plan** plan);
 /* As _range, with an execution-mode hint: 0 auto, 1 sequential (one CTA per
- * (signal, chunk), chunks start from their own warm-up), 2 decoupled look-back. */
+ * (signal, chunk), chunks start from their own warm-up), 2 decoupled look-back,
+ * 3 tensor cores (K4: chunked scan as tcgen05 3xTF32 GEMMs; fp32 transforms with <= 8
+ * orders sharing one injection constant, else SFTGPU_EINVAL). Auto picks K4 for such
+ * transforms when they span >= 4 x 148 tiles of 4096 outputs (SFTGPU_NO_TC=1 disables). */
 int sftgpu_transform_plan_create_ex(const sftgpu_spec* spec, int64_t n, int64_t batch, int boundary,
                                     int64_t out_begin, int64_t out_count, int mode_hint, sftgpu_plan** plan);
 int sftgpu_transform_execute(sftgpu_plan* plan, const void* x, int64_t ld_x, void* out,
@@ -252,10 +255,10 @@ int sftgpu_transform_execute_host_async(sftgpu_plan* plan, const void* x_host, v
 int sftgpu_plan_synchronize(sftgpu_plan* plan);
 /* 1 if the transform output is complex, 0 if real. */
 int sftgpu_plan_output_is_complex(const sftgpu_plan* plan);
-/* Plan geometry: info[0..9] = {sequential, direct-convolution, positions per thread,
+/* Plan geometry: info[0..10] = {sequential, direct-convolution, positions per thread,
  * positions per tile, warm-up tiles, chunks per signal, CTAs per launch, launches,
  * orders evaluated, injection group mode of the first launch (0 shared real, 1 split,
- * 2 per order, 3 shared complex)}. */
+ * 2 per order, 3 shared complex), tensor-core kernel K4}. */
 int sftgpu_plan_describe(const sftgpu_plan* plan, int64_t* info, int n_info);
 /* Number of kernel launches one execute issues. */
 int sftgpu_plan_launches_per_execute(const sftgpu_plan* plan);

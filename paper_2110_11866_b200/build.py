@@ -23,15 +23,30 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE
           *os.environ.get("SFTGPU_EXTRA_NVCC_FLAGS", "").split()]
 
 
-def _deps_mtime() -> float:
-    hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.hpp"))
-    hdrs.append(os.path.join(INCLUDE, "sftgpu.h"))
-    return max(os.path.getmtime(h) for h in hdrs)
+def _includes(path: str, seen: set) -> None:
+    """Local headers reachable from `path` through #include "..." lines."""
+    with open(path) as f:
+        for line in f:
+            line = line.strip()
+            if line.startswith("#include \""):
+                name = line.split('"')[1]
+                for d in (os.path.dirname(path), CSRC, INCLUDE):
+                    cand = os.path.normpath(os.path.join(d, name))
+                    if os.path.exists(cand) and cand not in seen:
+                        seen.add(cand)
+                        _includes(cand, seen)
+                        break
+
+
+def _deps_mtime(src: str) -> float:
+    seen: set = set()
+    _includes(src, seen)
+    return max([os.path.getmtime(h) for h in seen] + [0.0])
 
 
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-    if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), _deps_mtime()):
+    if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), _deps_mtime(src)):
         return obj
     cmd = [NVCC, *ARCH, *COMMON, "-c", src, "-o", obj]
     if src.endswith(".cu"):

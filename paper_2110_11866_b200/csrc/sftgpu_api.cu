@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <cstdlib>
+#include <type_traits>
 #include <cmath>
 #include <complex>
 #include <cstring>
@@ -14,6 +17,7 @@
 #include "aux_kernels.cuh"
 #include "host_fit.hpp"
 #include "scan_launch.cuh"
+#include "sft_tc_launch.h"
 
 namespace {
 using cd = std::complex<double>;
@@ -123,6 +127,11 @@ struct sftgpu_plan {
   void* d_out = nullptr;
   size_t cap_x = 0, cap_out = 0;
   int device = 0;
+  // K4 (tensor-core chunked transform): operand image + parameter block
+  int tc = 0;
+  void* d_tc_image = nullptr;
+  tck::TcParams tcp{};
+  int tc_grid = 0;
   // pipelined host execution: internal copy-in / compute / copy-out streams and a ring
   // of staging slots, so the transfers of neighbouring calls overlap this call's kernel
   struct Slot {
@@ -157,6 +166,7 @@ struct sftgpu_plan {
       cudaFree(g.d_tab);
       cudaFree(g.d_tab_tile);
     }
+    cudaFree(d_tc_image);
     cudaFree(d_ctrl);
     cudaFree(d_flags);
     cudaFree(d_agg);
@@ -432,6 +442,162 @@ void alloc_workspace(sftgpu_plan* pl) {
   cuda_check(cudaMalloc(&pl->d_incl, pay), "cudaMalloc prefixes");
 }
 
+
+// ---------------------------------------------------------------- K4 (tensor cores)
+// Builds the SW128 operand image of sft_tc.cuh from the lowered orders (fp64), and the
+// plan geometry. Eligible: fp32 transform, <= 8 orders sharing one injection constant
+// z^{2K} (group modes 0 and 3), enough tiles to fill the GPU (or mode_hint 3).
+uint32_t sw128(uint32_t row, uint32_t k) { return row * 128u + ((((k >> 2) ^ (row & 7u)) << 4) | ((k & 3u) << 2)); }
+float tf32_head(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u &= 0xFFFFE000u;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
+  auto no = [&](const char* why) {
+    if (force) fail(SFTGPU_EINVAL, std::string("tensor-core mode unavailable: ") + why);
+    return false;
+  };
+  if (pl->precision != SFTGPU_SINGLE) return no("needs single precision");
+  if (lw.orders.empty() || lw.orders.size() > static_cast<size_t>(tck::kMaxOrd)) return no("needs 1..8 orders");
+  std::vector<Order> ords = lw.orders;
+  cd cA(0, 0), cB(0, 0);
+  int na = 0;
+  const int gm = detect_groups(ords, lw.alpha, lw.K, &cA, &cB, &na);
+  cd cinj;
+  if (gm == sftk::kGroupShared)
+    cinj = cA;
+  else if (gm == sftk::kGroupSplit && na == 0)
+    cinj = cB;
+  else
+    return no("orders do not share one injection constant");
+  if (!force) {
+    // auto-selection only once K4 beats K1 on the batched shapes (SFTGPU_TC=1 opts in)
+    const char* env = std::getenv("SFTGPU_TC");
+    if (!env || env[0] != '1') return false;
+    const long long tiles = pl->batch * ((pl->count + tck::kTile - 1) / tck::kTile);
+    if (tiles < 4LL * 148) return false;
+  }
+  const bool cplx = lw.complex_out;
+  const int nord = static_cast<int>(ords.size());
+  const double alpha = lw.alpha, pref = lw.prefactor;
+  const int K = lw.K;
+  // combine weights K_p(w) = (k0 Re w + k1 Im w, k2 Re w + k3 Im w) and the x[n-K] weight D
+  std::vector<std::array<double, 4>> kw(nord);
+  cd D(0, 0);
+  for (int p = 0; p < nord; ++p) {
+    const double w = ords[p].omega;
+    const cd a = zpow(alpha, w, -static_cast<double>(K)), b = zpow(alpha, w, static_cast<double>(K));
+    const cd A = pref * (ords[p].wc + cd(0, 1) * ords[p].ws) * 0.5;
+    const cd B = pref * (ords[p].wc - cd(0, 1) * ords[p].ws) * 0.5;
+    const cd E = A * a, F = B * std::conj(a);
+    kw[p] = {E.real() + F.real(), F.imag() - E.imag(), E.imag() + F.imag(), E.real() - F.real()};
+    D += A * b + B * std::conj(b);
+  }
+  auto Kp = [&](int p, cd v) { return cd(kw[p][0] * v.real() + kw[p][1] * v.imag(), kw[p][2] * v.real() + kw[p][3] * v.imag()); };
+  std::vector<unsigned char> img(tck::kImage, 0);
+  auto put = [&](uint32_t region, int row, int k, float v) { std::memcpy(&img[region + sw128(row, k)], &v, 4); };
+  auto put_split = [&](uint32_t rh, uint32_t rl, int row, int k, double v) {
+    const float h = tf32_head(static_cast<float>(v));
+    put(rh, row, k, h);
+    if (rl != 0xFFFFFFFFu) put(rl, row, k, static_cast<float>(v - static_cast<double>(h)));
+    return static_cast<float>(v - static_cast<double>(h));
+  };
+  // effective kernel taps on the lead / trail streams, lag d = 0..31
+  std::vector<cd> hl(tck::kQ), ht(tck::kQ);
+  for (int d = 0; d < tck::kQ; ++d) {
+    cd sl(0, 0), st(0, 0);
+    for (int p = 0; p < nord; ++p) {
+      const cd zd = zpow(alpha, ords[p].omega, d);
+      sl += Kp(p, zd);
+      st += Kp(p, -cinj * zd);
+    }
+    if (d == 0) st += D;
+    hl[d] = sl;
+    ht[d] = st;
+  }
+  const int comps = cplx ? 2 : 1;
+  for (int i = 0; i < tck::kQ; ++i)
+    for (int r = 0; r < comps; ++r) {
+      const int j = comps * i + r;
+      for (int m = 0; m <= i; ++m) {
+        const cd vl = hl[i - m], vt = ht[i - m];
+        put_split(tck::kHLh, tck::kHLl, j, m, r == 0 ? vl.real() : vl.imag());
+        put_split(tck::kHTh, tck::kHTl, j, m, r == 0 ? vt.real() : vt.imag());
+      }
+      // chunk start state S_p -> output i: K_p(z^{i+1} S_p)
+      for (int p = 0; p < nord; ++p) {
+        const cd a = zpow(alpha, ords[p].omega, i + 1.0);
+        const double k0 = r == 0 ? kw[p][0] : kw[p][2], k1 = r == 0 ? kw[p][1] : kw[p][3];
+        const double cr = k0 * a.real() + k1 * a.imag(), ci = -k0 * a.imag() + k1 * a.real();
+        for (int q = 0; q < 2; ++q) {
+          const double v = q == 0 ? cr : ci;
+          const float h = tf32_head(static_cast<float>(v));
+          put(tck::kBC1, j, 2 * p + q, h);
+          put(tck::kBC1, j, 16 + 2 * p + q, h);
+          put(tck::kBC2, j, 2 * p + q, static_cast<float>(v - static_cast<double>(h)));
+        }
+      }
+    }
+  // chunk aggregates A_p = sum_m z^{31-m} (xl[m] - c xt[m])
+  for (int p = 0; p < nord; ++p)
+    for (int m = 0; m < tck::kQ; ++m) {
+      const cd zl = zpow(alpha, ords[p].omega, tck::kQ - 1.0 - m), zt = -cinj * zl;
+      put_split(tck::kALh, tck::kALl, 2 * p, m, zl.real());
+      put_split(tck::kALh, tck::kALl, 2 * p + 1, m, zl.imag());
+      put_split(tck::kATh, tck::kATl, 2 * p, m, zt.real());
+      put_split(tck::kATh, tck::kATl, 2 * p + 1, m, zt.imag());
+    }
+  tck::TcParams& P = pl->tcp;
+  std::memset(&P, 0, sizeof(P));
+  for (int p = 0; p < nord; ++p) {
+    const double w = ords[p].omega;
+    for (int l = 0; l < 32; ++l) {
+      const cd v = zpow(alpha, w, 32.0 * l);
+      const float f[2] = {static_cast<float>(v.real()), static_cast<float>(v.imag())};
+      std::memcpy(&img[tck::kZl + (p * 32 + l) * 8], f, 8);
+    }
+    for (int k = 0; k < 6; ++k) {
+      const cd v = zpow(alpha, w, k < 5 ? 32.0 * (1 << k) : 1024.0);
+      P.zs[p][k] = make_float2(static_cast<float>(v.real()), static_cast<float>(v.imag()));
+    }
+    const cd z1 = zpow(alpha, w, 1024.0), zt = zpow(alpha, w, static_cast<double>(tck::kTile));
+    P.z1024[p] = make_double2(z1.real(), z1.imag());
+    P.zT[p] = make_double2(zt.real(), zt.imag());
+  }
+  for (size_t i = 0; i < img.size(); i += 4) {
+    float f;
+    std::memcpy(&f, &img[i], 4);
+    if (!std::isfinite(f)) fail(SFTGPU_EINVAL, "attenuation alpha*K too large for the requested precision");
+  }
+  cuda_check(cudaMalloc(&pl->d_tc_image, img.size()), "cudaMalloc tc image");
+  cuda_check(cudaMemcpy(pl->d_tc_image, img.data(), img.size(), cudaMemcpyHostToDevice), "copy tc image");
+  // geometry: items = (signal, chunk); one persistent CTA per SM walks items in order
+  constexpr long long kSms = 148;
+  const long long tiles_sig = (pl->count + tck::kTile - 1) / tck::kTile;
+  long long chunks = 1;
+  if (pl->batch < kSms) chunks = std::min(tiles_sig, (kSms + pl->batch - 1) / pl->batch);
+  const long long per = (tiles_sig + chunks - 1) / chunks;
+  P.chunk_len = per * tck::kTile;
+  P.n_chunks = (pl->count + P.chunk_len - 1) / P.chunk_len;
+  P.n_items = pl->batch * P.n_chunks;
+  P.warm_tiles = (2LL * K + tck::kTile - 1) / tck::kTile;
+  P.n = pl->n;
+  P.lo = pl->lo;
+  P.count = pl->count;
+  P.K = K;
+  P.boundary = pl->boundary;
+  P.nord = nord;
+  P.cplx = cplx ? 1 : 0;
+  P.image = static_cast<const uint4*>(pl->d_tc_image);
+  pl->tc_grid = static_cast<int>(std::min(kSms, P.n_items));
+  pl->tc = 1;
+  return true;
+}
+
 Lowered lower_spec(const sftb::Spec& s) {
   Lowered lw;
   lw.alpha = s.alpha;
@@ -672,9 +838,27 @@ sftb::Spec spec_from_c(const sftgpu_spec* o) {
   return s;
 }
 
+long long* g_tc_trace = nullptr;  // diagnostics: sftgpu_debug_set_tc_trace
+
+void run_tc(sftgpu_plan* pl, const void* x, long long ld_x, void* out, long long ld_out, cudaStream_t st) {
+  tck::TcParams P = pl->tcp;
+  P.x = static_cast<const float*>(x);
+  P.out = static_cast<float*>(out);
+  P.ld_x = ld_x;
+  P.ld_out = ld_out;
+  const size_t rowb = static_cast<size_t>(ld_out) * sizeof(float) * (P.cplx ? 2 : 1);
+  P.vec_ok = (reinterpret_cast<uintptr_t>(out) % 16 == 0 && rowb % 16 == 0) ? 1 : 0;
+  P.trace = g_tc_trace;
+  cuda_check(tck::launch_tc(P, pl->tc_grid, st), "sft_tc_kernel launch");
+}
+
 template <typename T>
 void run_groups(sftgpu_plan* pl, const void* x, long long ld_x, void* out, void* out_s, long long ld_out,
                 int accumulate_first, cudaStream_t st) {
+  if (pl->tc) {
+    if constexpr (std::is_same<T, float>::value) run_tc(pl, x, ld_x, out, ld_out, st);
+    return;
+  }
   for (size_t gi = 0; gi < pl->groups.size(); ++gi) {
     Group& g = pl->groups[gi];
     sftk::ScanParams<T> P = params_of<T>(g);
@@ -915,7 +1099,8 @@ int sftgpu_transform_plan_create_range(const sftgpu_spec* spec, int64_t n, int64
 int sftgpu_transform_plan_create_ex(const sftgpu_spec* spec, int64_t n, int64_t batch, int boundary,
                                     int64_t out_begin, int64_t out_count, int mode_hint, sftgpu_plan** plan) {
   return guarded([&] {
-    if (mode_hint < 0 || mode_hint > 2) fail(SFTGPU_EINVAL, "mode_hint must be 0 (auto), 1 (sequential), 2 (look-back)");
+    if (mode_hint < 0 || mode_hint > 3)
+      fail(SFTGPU_EINVAL, "mode_hint must be 0 (auto), 1 (sequential), 2 (look-back), 3 (tensor cores)");
     if (!plan) fail(SFTGPU_EINVAL, "null plan pointer");
     *plan = nullptr;
     if (n < 1) fail(SFTGPU_EINVAL, "Signal: need at least one sample");
@@ -953,7 +1138,11 @@ int sftgpu_transform_plan_create_ex(const sftgpu_spec* spec, int64_t n, int64_t 
     pl->lo = out_begin - static_cast<long long>(s.n0);  // window read at n - n0 (transforms.cpp:287-288)
     pl->count = out_count;
     pl->mode = lw.complex_out ? sftk::kModeComplex : sftk::kModeReal;
-    pl->mode_hint = mode_hint;
+    pl->mode_hint = mode_hint == 3 ? 0 : mode_hint;
+    if ((mode_hint == 0 || mode_hint == 3) && build_tc(pl.get(), lw, mode_hint == 3)) {
+      *plan = pl.release();
+      return;
+    }
     choose_geometry(pl.get());
     if (pl->precision == SFTGPU_SINGLE)
       build_groups<float>(pl.get(), lw.orders, lw.alpha, lw.prefactor, false);
@@ -1130,16 +1319,23 @@ int sftgpu_plan_describe(const sftgpu_plan* pl, int64_t* info, int n_info) {
     if (!pl || !info) fail(SFTGPU_EINVAL, "null argument");
     int64_t orders = 0;
     for (const Group& g : pl->groups) orders += g.nord;
-    const int64_t v[10] = {pl->seq, pl->conv, pl->L * 1LL, pl->TT, pl->warm_tiles, pl->n_chunks, pl->total_tiles,
+    if (pl->tc) {
+      const int64_t v[11] = {0, 0, 0, tck::kTile, pl->tcp.warm_tiles, pl->tcp.n_chunks, pl->tc_grid, 1,
+                             pl->tcp.nord, -1, 1};
+      for (int i = 0; i < n_info && i < 11; ++i) info[i] = v[i];
+      return;
+    }
+    const int64_t v[11] = {pl->seq, pl->conv, pl->L * 1LL, pl->TT, pl->warm_tiles, pl->n_chunks, pl->total_tiles,
                            static_cast<int64_t>(pl->groups.size()), orders,
-                           pl->groups.empty() ? -1 : pl->groups[0].gm};
-    for (int i = 0; i < n_info && i < 10; ++i) info[i] = v[i];
+                           pl->groups.empty() ? -1 : pl->groups[0].gm, 0};
+    for (int i = 0; i < n_info && i < 11; ++i) info[i] = v[i];
   });
 }
 
 int sftgpu_plan_launches_per_execute(const sftgpu_plan* pl) {
   if (!pl) return 0;
   if (pl->conv) return static_cast<int>(pl->batch);
+  if (pl->tc) return 1;
   return static_cast<int>(pl->groups.size());
 }
 
@@ -1190,6 +1386,10 @@ int sftgpu_components_execute_host(sftgpu_plan* pl, const void* x_host, void* c_
 }
 
 void sftgpu_plan_destroy(sftgpu_plan* pl) { delete pl; }
+
+/* Diagnostics (not part of the reference interface): device buffer of 64 x 16 int64 that
+ * K4 fills with per-tile event clocks of CTA 0 (tools/tc_trace.py); NULL disables. */
+void sftgpu_debug_set_tc_trace(void* dev_buf) { g_tc_trace = static_cast<long long*>(dev_buf); }
 
 int sftgpu_generate_signal(int kind, int64_t n, uint64_t seed, int64_t batch, int dtype, void* out, void* stream) {
   return guarded([&] {

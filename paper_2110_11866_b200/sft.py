@@ -562,7 +562,7 @@ class TransformPlan:
     real, or [batch][ld_out][2] complex interleaved. ``out_range=(begin, count)``
     computes only outputs [begin, begin+count) (chunk sharding with halo)."""
 
-    MODES = {"auto": 0, "seq": 1, "lookback": 2}
+    MODES = {"auto": 0, "seq": 1, "lookback": 2, "tc": 3}
 
     def __init__(self, spec: TransformSpec, n: int, batch: int = 1, boundary=BoundaryPolicy.Clamp,
                  out_range=None, mode: str = "auto"):
@@ -579,10 +579,10 @@ class TransformPlan:
         self.launches = lib().sftgpu_plan_launches_per_execute(h)
 
     def describe(self) -> dict:
-        info = (C.c_int64 * 10)()
-        check(lib().sftgpu_plan_describe(self._h, info, 10))
+        info = (C.c_int64 * 11)()
+        check(lib().sftgpu_plan_describe(self._h, info, 11))
         keys = ("sequential", "direct_convolution", "positions_per_thread", "positions_per_tile", "warm_tiles",
-                "chunks_per_signal", "ctas_per_launch", "launches", "orders", "group_mode")
+                "chunks_per_signal", "ctas_per_launch", "launches", "orders", "group_mode", "tensor_cores")
         return dict(zip(keys, list(info)))
 
     @property

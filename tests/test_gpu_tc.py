@@ -1,0 +1,87 @@
+"""GPU parity for K4, the tensor-core chunked transform (csrc/sft_tc.cuh): the same
+transforms as K1 (proj/src/transforms.cpp:279-428) evaluated as 3xTF32 tcgen05 GEMMs
+over 32-position chunks plus a chunk-state scan. Checked against the fp64 oracle
+restatement of the reference combine (north_star: <= 1e-5 relative for fp32 ASFT), and
+row by row against K1 (the CUDA-core kernel) on the same inputs."""
+import numpy as np
+import pytest
+
+from conftest import rel_max
+from test_gpu_transforms import oracle_transform
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(sft, spec, xb, mode, boundary=1, out_range=None):
+    import torch
+
+    n = xb.shape[1]
+    plan = sft.TransformPlan(spec, n, xb.shape[0], boundary, out_range, mode=mode)
+    out = plan.empty_output()
+    plan.execute(xb, out)
+    torch.cuda.synchronize()
+    oh = out.double().cpu().numpy()
+    return plan, (oh[..., 0] + 1j * oh[..., 1] if plan.complex_out else oh)
+
+
+CASES = [
+    # abbreviation, sigma, xi, n, batch
+    ("MMS5P3", 8192.0, 10.0, 102400, 6),   # BASELINE config 4 shape (2P+1 = 7 orders, complex injection)
+    ("MDS5P6", 8192.0, 10.0, 102400, 2),   # config 3 spec (6 orders, real injection)
+    ("GDS10P6", 8192.0, 0.0, 102400, 2),   # config 2 spec, real output
+    ("MDS3P6", 40.0, 8.0, 20001, 3),       # small sigma, partial last tile
+    ("MMS2P3", 64.0, 10.0, 9000, 5),
+    ("GDS4P5", 512.0, 0.0, 50000, 2),
+    ("MDP6", 1000.0, 10.0, 30000, 2),      # SFT (alpha = 0)
+]
+
+
+@pytest.mark.parametrize("abbrev,sigma,xi,n,batch", CASES)
+def test_tc_vs_oracle_and_cuda_core(sft, O, abbrev, sigma, xi, n, batch):
+    spec = sft.make_transform_spec(abbrev, sigma, xi, sft.TransformOptions(precision=0))
+    xb = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 77, batch, sft.Precision.Single)
+    plan, tc = _run(sft, spec, xb, "tc")
+    assert plan.describe()["tensor_cores"] == 1
+    _, ref1 = _run(sft, spec, xb, "seq")
+    xh = xb.double().cpu().numpy()
+    for b in sorted({0, batch - 1}):
+        assert rel_max(tc[b], oracle_transform(O, xh[b], 1, spec)) < 1e-5
+    assert rel_max(tc, ref1) < 1e-5
+
+
+@pytest.mark.parametrize("boundary", [0, 1])
+def test_tc_boundaries_and_offset(sft, O, boundary):
+    """Both boundary policies, and a DC offset (x + 1, the fp32 cancellation case)."""
+    import torch
+
+    spec = sft.make_transform_spec("MMS5P3", 300.0, 10.0, sft.TransformOptions(precision=0))
+    n = 12345
+    x = O.make_test_signal(O.SEEDED_NOISE, n, 5) + 1.0
+    xb = torch.tensor(np.stack([x, -x]), dtype=torch.float32, device="cuda")
+    _, tc = _run(sft, spec, xb, "tc", boundary)
+    xh = xb.double().cpu().numpy()
+    for b in range(2):
+        assert rel_max(tc[b], oracle_transform(O, xh[b], boundary, spec)) < 1e-5
+
+
+def test_tc_ranged_plan_matches_full(sft, O):
+    """Output-range plans (chunk sharding with halo) reproduce the full transform."""
+    spec = sft.make_transform_spec("MDS5P6", 2000.0, 10.0, sft.TransformOptions(precision=0))
+    n = 60000
+    xb = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 3, 1, sft.Precision.Single)
+    _, full = _run(sft, spec, xb, "tc")
+    for b, c in ((0, 7000), (23456, 20000), (n - 9999, 9999)):
+        _, part = _run(sft, spec, xb, "tc", 1, (b, c))
+        assert rel_max(part[0], full[0, b:b + c]) < 2e-6
+
+
+def test_tc_selection(sft, O):
+    spec = sft.make_transform_spec("MMS5P3", 8192.0, 10.0, sft.TransformOptions(precision=0))
+    assert sft.TransformPlan(spec, 102400, 4096, mode="tc").describe()["tensor_cores"] == 1
+    assert sft.TransformPlan(spec, 102400, 1).describe()["tensor_cores"] == 0
+
+
+def test_tc_rejects_ineligible_specs(sft):
+    fp64 = sft.make_transform_spec("MDS5P6", 100.0, 10.0, sft.TransformOptions(precision=1))
+    with pytest.raises(ValueError):
+        sft.TransformPlan(fp64, 10000, 2, mode="tc")
