@@ -18,17 +18,24 @@
 // Precision: operands are split x = hi + lo with hi the TF32 head; each product is
 // hi*hi + lo*hi + hi*lo (3xTF32), fp32 accumulation in TMEM (~1e-6 relative).
 //
-// Roles (one persistent CTA per SM, 448 threads):
-//   warps 0-3   chunk-state scan (thread = chunk = TMEM lane); warm-up tiles only reduce
-//               their aggregates into the fp64 tile carry
-//   warps 4-7   epilogue: TMEM -> registers -> swizzled staging -> coalesced 16-byte stores
-//   warps 8-11  loader: cp.async (LDGSTS) of the raw samples straight into the SW128 hi
-//               tiles (the MMA reads them as TF32 heads), then the fp32 remainders into
-//               the lo tiles; boundary segments by value
-//   warps 12-13 MMA issuers (GEMM1 of every tile / GEMM2 of every output tile)
-// Pipelines (mbarriers): X tiles double-buffered, GEMM1/GEMM2 accumulators
-// double-buffered in TMEM, chunk-state operand single-buffered, tile carry
-// double-buffered.
+// Operand placement: the signal tiles and the chunk states are A operands held in TMEM
+// (lane = chunk, column = position), so shared memory only feeds the small coefficient
+// B operands; GEMM1 rides along GEMM2 as 16 extra N columns (B rows [outputs ;
+// aggregates]), and the chunk-state product is a second short MMA chain into the same
+// accumulator once the scan has produced the states.
+//
+// Roles (one persistent CTA per SM, 512 threads):
+//   warps 0-7   chunk-state scan (thread = chunk = TMEM lane; warps 0-3 take the first
+//               half of the orders, warps 4-7 the rest) -> states into TMEM, then warp 0
+//               issues the chunk-state GEMM; warm-up tiles only reduce their aggregates
+//               into the fp64 tile carry
+//   warps 8-11  epilogue: TMEM -> swizzled staging (accumulator released) -> coalesced
+//               16-byte stores
+//   warps 12-15 loader: coalesced cp.async into a ring of padded staging rows; each
+//               thread then reads its chunk row, splits it (TF32 head / remainder) and
+//               tcgen05.st's it; warp 12 then issues the merged GEMM of the tile
+// Pipelines (mbarriers): TMEM X operands, chunk states and accumulators double-buffered;
+// loader staging ring; tile carry double-buffered.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -41,10 +48,10 @@
 namespace tck {
 
 struct Misc {
-  uint64_t xfull[2], xfree[2], g1done[2], d1free[2], g2done[2], d2free[2], ssfull;
+  uint64_t xfree[2], g1done[2], dfree[2], g2done[2];
   uint32_t tmem;
-  double2 cy[2][kMaxOrd];     // tile carry (state entering the tile), fp64, by tile parity
-  float2 wtot[2][4][kMaxOrd]; // per-warp chunk-aggregate totals (by tile parity)
+  double2 cy[2][kMaxOrd];      // tile carry (state entering the tile), fp64, by tile parity
+  float2 wtot[2][4][kMaxOrd];  // per-warp chunk-aggregate totals (by tile parity)
 };
 
 // (item, tile) walk shared by every role
@@ -75,6 +82,9 @@ struct Walk {
   __device__ bool last(const TcParams& P) const { return t + 1 == ntiles; }
 };
 
+__device__ __forceinline__ void trace_ev(const TcParams& P, long long gt, int ev) {
+  if (P.trace && blockIdx.x == 0 && gt < 64) P.trace[gt * 16 + ev] = clock64();
+}
 
 __device__ __forceinline__ float tf32_lo(float v) { return v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
 
@@ -83,54 +93,7 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const float* src, unsign
                : "memory");
 }
 
-// Stage one stream of a tile: element e = lt + 128 r (warp-coalesced) -> (row e / 32,
-// column e % 32) of the SW128 hi/lo tiles. Returns true when the samples are in flight
-// (cp.async into the hi tile; lo tile pending), false when both tiles were written.
-// Segment classes as in K1's stage_stream: inside the signal, one uniform boundary
-// value (before the warm start: zeros; clamp region: the edge sample), or straddling.
-__device__ __forceinline__ bool stage_stream(const TcParams& P, const float* xs, long long j0, long long jmin, int lt,
-                                             unsigned long long pol, unsigned char* hi, unsigned char* lo) {
-  const long long n = P.n;
-  const uint32_t hs = umma::smem_u32(hi);
-  if (j0 >= jmin && j0 >= 0 && j0 + kTile <= n) {
-    const float* p = xs + j0 + lt;
-#pragma unroll
-    for (int r = 0; r < 32; ++r)
-      cp_async4(hs + umma::sw128_off(static_cast<uint32_t>((lt >> 5) + 4 * r), static_cast<uint32_t>(lt & 31)),
-                p + 128 * r, pol);
-    return true;
-  }
-  if (j0 + kTile <= jmin || (j0 >= jmin && (j0 >= n || j0 + kTile <= 0))) {
-    float v = 0.f;
-    if (j0 + kTile > jmin && P.boundary != 0) v = __ldg(xs + (j0 >= n ? n - 1 : 0));
-    const float l = tf32_lo(v);
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const uint32_t off = umma::sw128_off(static_cast<uint32_t>((lt >> 5) + 4 * r), static_cast<uint32_t>(lt & 31));
-      *reinterpret_cast<float*>(hi + off) = v;
-      *reinterpret_cast<float*>(lo + off) = l;
-    }
-    return false;
-  }
-  float v[32];
-#pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    const long long j = j0 + lt + 128 * r;
-    const long long jc = j < 0 ? 0 : (j >= n ? n - 1 : j);
-    v[r] = __ldg(xs + jc);
-  }
-#pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    const long long j = j0 + lt + 128 * r;
-    if (j < jmin || (P.boundary == 0 && (j < 0 || j >= n))) v[r] = 0.f;
-    const uint32_t off = umma::sw128_off(static_cast<uint32_t>((lt >> 5) + 4 * r), static_cast<uint32_t>(lt & 31));
-    *reinterpret_cast<float*>(hi + off) = v[r];
-    *reinterpret_cast<float*>(lo + off) = tf32_lo(v[r]);
-  }
-  return false;
-}
-
-// bulk L2 prefetch of the 16 KB a tile stream reads (clipped to the signal, 16-B aligned)
+// bulk L2 prefetch of the samples a tile stream reads (clipped to the signal, 16-B aligned)
 __device__ __forceinline__ void prefetch_l2(const float* xs, long long j0, long long n) {
   long long a = j0 < 0 ? 0 : j0, e = j0 + kTile > n ? n : j0 + kTile;
   if (e <= a) return;
@@ -140,75 +103,97 @@ __device__ __forceinline__ void prefetch_l2(const float* xs, long long j0, long 
                : "memory");
 }
 
-// lo tile from the landed hi tile (this thread's own elements; all loads before the
-// stores, so they overlap instead of serialising on possible aliasing)
-__device__ __forceinline__ void finish_lo(const unsigned char* hi, unsigned char* lo, int lt) {
+// Boundary segments of stage_rows (kept out of line: cold code, small hot loop)
+__device__ __noinline__ void stage_rows_edge(const TcParams& P, const float* xs, long long j0, long long jmin,
+                                             int lane, float* stg) {
+  const long long n = P.n;
+  constexpr int kSeg = 32 * kQ;
+  if (j0 + kSeg <= jmin || (j0 >= jmin && (j0 >= n || j0 + kSeg <= 0))) {
+    float v = 0.f;
+    if (j0 + kSeg > jmin && P.boundary != 0) v = __ldg(xs + (j0 >= n ? n - 1 : 0));
+    for (int r = 0; r < 32; ++r) stg[r * kStgRow + lane] = v;
+    return;
+  }
   float v[32];
 #pragma unroll
-  for (int r = 0; r < 32; ++r)
-    v[r] = *reinterpret_cast<const float*>(
-        hi + umma::sw128_off(static_cast<uint32_t>((lt >> 5) + 4 * r), static_cast<uint32_t>(lt & 31)));
+  for (int r = 0; r < 32; ++r) {
+    const long long j = j0 + kQ * r + lane;
+    v[r] = __ldg(xs + (j < 0 ? 0 : (j >= n ? n - 1 : j)));
+  }
 #pragma unroll
-  for (int r = 0; r < 32; ++r)
-    *reinterpret_cast<float*>(lo + umma::sw128_off(static_cast<uint32_t>((lt >> 5) + 4 * r),
-                                                   static_cast<uint32_t>(lt & 31))) = tf32_lo(v[r]);
+  for (int r = 0; r < 32; ++r) {
+    const long long j = j0 + kQ * r + lane;
+    if (j < jmin || (P.boundary == 0 && (j < 0 || j >= n))) v[r] = 0.f;
+    stg[r * kStgRow + lane] = v[r];
+  }
 }
 
-__device__ __forceinline__ void trace_ev(const TcParams& P, long long gt, int ev) {
-  if (P.trace && blockIdx.x == 0 && gt < 64) P.trace[gt * 16 + ev] = clock64();
+// Stage one stream of this warp's 32 chunk rows: row r = samples j0 + 32 r + [0, 32),
+// lane l loads column l (warp-coalesced) into the padded staging rows. Segment classes as
+// in K1's stage_stream: inside the signal (cp.async), or a boundary segment (uniform
+// boundary value, or straddling an edge / the warm start: per element).
+__device__ __forceinline__ void stage_rows(const TcParams& P, const float* xs, long long j0, long long jmin, int lane,
+                                           unsigned long long pol, float* stg) {
+  constexpr int kSeg = 32 * kQ;
+  if (j0 >= jmin && j0 >= 0 && j0 + kSeg <= P.n) {
+    const uint32_t s0 = umma::smem_u32(stg) + 4u * static_cast<uint32_t>(lane);
+    const float* p = xs + j0 + lane;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) cp_async4(s0 + r * kStgRow * 4, p + kQ * r, pol);
+    return;
+  }
+  stage_rows_edge(P, xs, j0, jmin, lane, stg);
 }
 
-__device__ __forceinline__ void bar_scan() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-__device__ __forceinline__ void bar_epi() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
+// this thread's chunk row from staging -> TMEM: head columns [col, +32), remainder [col+32, +32)
+__device__ __forceinline__ void row_to_tmem(const float* stg, int lane, uint32_t taddr) {
+  uint32_t h[32], l[32];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 v = *reinterpret_cast<const float4*>(stg + lane * kStgRow + 4 * j);
+    h[4 * j] = __float_as_uint(v.x);
+    h[4 * j + 1] = __float_as_uint(v.y);
+    h[4 * j + 2] = __float_as_uint(v.z);
+    h[4 * j + 3] = __float_as_uint(v.w);
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) l[i] = __float_as_uint(tf32_lo(__uint_as_float(h[i])));
+  umma::tmem_st32(taddr, h);
+  umma::tmem_st32(taddr + 32, l);
+}
+
+__device__ __noinline__ void store_masked(float* dst, float4 val, long long pos, long long cnt, int cw) {
+  const float e[4] = {val.x, val.y, val.z, val.w};
+  for (int j = 0; j < 4; ++j)
+    if (pos + j / cw < cnt) dst[j] = e[j];
+}
+
+// named barriers: scan order-sets (1, 2), epilogue (3), loader (4), all scan warps (5)
+__device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __device__ __forceinline__ float2 cmla(float2 z, float2 t, float2 a) {  // a + z t
   return make_float2(fmaf(z.x, t.x, fmaf(-z.y, t.y, a.x)), fmaf(z.x, t.y, fmaf(z.y, t.x, a.y)));
 }
 
-template <int B, int K>
-__device__ __forceinline__ void gemm1_k(uint64_t db, uint32_t d, uint32_t id, bool trail) {
-  constexpr uint32_t x0 = kX + B * 4 * kXT, ko = 32 * K;
-  umma::mma_tf32_off<x0 + ko, kALh + ko>(d, db, id, K > 0);
-  umma::mma_tf32_off<x0 + kXT + ko, kALh + ko>(d, db, id, 1);
-  umma::mma_tf32_off<x0 + ko, kALl + ko>(d, db, id, 1);
-  if (trail) {
-    umma::mma_tf32_off<x0 + 2 * kXT + ko, kATh + ko>(d, db, id, 1);
-    umma::mma_tf32_off<x0 + 3 * kXT + ko, kATh + ko>(d, db, id, 1);
-    umma::mma_tf32_off<x0 + 2 * kXT + ko, kATl + ko>(d, db, id, 1);
-  }
+// ---- MMA chains (warp-uniform; B at compile-time offsets from the descriptor base)
+// Merged GEMM1 + GEMM2a of an output tile: D[:, 0:NO+16) = X . [B_out ; B_agg]^T (3xTF32)
+template <int K>
+__device__ __forceinline__ void merged_k(uint64_t db, uint32_t d, uint32_t x, uint32_t id) {
+  constexpr uint32_t ko = 32 * K;
+  umma::mma_tf32_ts<kBLh + ko>(d, x + 8 * K, db, id, K > 0);        // xl_h . BL_h
+  umma::mma_tf32_ts<kBLh + ko>(d, x + 32 + 8 * K, db, id, 1);       // xl_l . BL_h
+  umma::mma_tf32_ts<kBLl + ko>(d, x + 8 * K, db, id, 1);            // xl_h . BL_l
+  umma::mma_tf32_ts<kBTh + ko>(d, x + 64 + 8 * K, db, id, 1);       // xt_h . BT_h
+  umma::mma_tf32_ts<kBTh + ko>(d, x + 96 + 8 * K, db, id, 1);       // xt_l . BT_h
+  umma::mma_tf32_ts<kBTl + ko>(d, x + 64 + 8 * K, db, id, 1);       // xt_h . BT_l
 }
-
-template <int B>
-__device__ __forceinline__ void gemm1(uint64_t db, uint32_t tmem, bool trail) {
-  const uint32_t d = tmem + 128 + 32 * B;
-  constexpr uint32_t id = umma::idesc_tf32(128, 16);
-  gemm1_k<B, 0>(db, d, id, trail);
-  gemm1_k<B, 1>(db, d, id, trail);
-  gemm1_k<B, 2>(db, d, id, trail);
-  gemm1_k<B, 3>(db, d, id, trail);
-}
-
-template <int B, int K>
-__device__ __forceinline__ void gemm2_k(uint64_t db, uint32_t d, uint32_t id) {
-  constexpr uint32_t x0 = kX + B * 4 * kXT, ko = 32 * K;
-  umma::mma_tf32_off<x0 + ko, kHLh + ko>(d, db, id, K > 0);
-  umma::mma_tf32_off<x0 + kXT + ko, kHLh + ko>(d, db, id, 1);
-  umma::mma_tf32_off<x0 + ko, kHLl + ko>(d, db, id, 1);
-  umma::mma_tf32_off<x0 + 2 * kXT + ko, kHTh + ko>(d, db, id, 1);
-  umma::mma_tf32_off<x0 + 3 * kXT + ko, kHTh + ko>(d, db, id, 1);
-  umma::mma_tf32_off<x0 + 2 * kXT + ko, kHTl + ko>(d, db, id, 1);
-  umma::mma_tf32_off<kSS + ko, kBC1 + ko>(d, db, id, 1);
-  if (K < 2) umma::mma_tf32_off<kSS + ko, kBC2 + ko>(d, db, id, 1);
-}
-
-template <int B, int D2>
-__device__ __forceinline__ void gemm2(uint64_t db, uint32_t tmem, int cplx) {
-  const uint32_t d = tmem + 64 * D2;
-  const uint32_t id = cplx ? umma::idesc_tf32(128, 64) : umma::idesc_tf32(128, 32);
-  gemm2_k<B, 0>(db, d, id);
-  gemm2_k<B, 1>(db, d, id);
-  gemm2_k<B, 2>(db, d, id);
-  gemm2_k<B, 3>(db, d, id);
+// Warm-up tile: aggregates only (lead stream; the trail is before the warm start)
+template <int K, uint32_t NO>
+__device__ __forceinline__ void warm_k(uint64_t db, uint32_t d, uint32_t x, uint32_t id) {
+  constexpr uint32_t ko = 32 * K, ro = NO * 128;
+  umma::mma_tf32_ts<kBLh + ro + ko>(d, x + 8 * K, db, id, K > 0);
+  umma::mma_tf32_ts<kBLh + ro + ko>(d, x + 32 + 8 * K, db, id, 1);
+  umma::mma_tf32_ts<kBLl + ro + ko>(d, x + 8 * K, db, id, 1);
 }
 
 template <int NORD>
@@ -218,203 +203,182 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
   Misc& M = *reinterpret_cast<Misc*>(sm + kMisc);
   const int tid = threadIdx.x, lane = tid & 31;
   // warp index as a provably warp-uniform value: role branches become uniform branches
-  // and the MMA issuers keep descriptors on the uniform datapath
+  // and the MMA issuer keeps descriptors on the uniform datapath
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int NO = P.cplx ? 2 * kQ : kQ;  // output columns of the accumulator
 
-  // ---- setup: operand image, barriers, TMEM (256 columns: D2 x2 at 0/64, D1 x2 at 128/160)
+  // ---- setup: operand image, barriers, TMEM (512 columns)
   {
     uint4* dst = reinterpret_cast<uint4*>(sm);
     for (int i = tid; i < static_cast<int>(kImage / 16); i += kThreads) dst[i] = __ldg(P.image + i);
   }
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
-      umma::mbar_init(&M.xfull[b], 128);
       umma::mbar_init(&M.xfree[b], 1);
       umma::mbar_init(&M.g1done[b], 1);
-      umma::mbar_init(&M.d1free[b], 128);
+      umma::mbar_init(&M.dfree[b], 128);
       umma::mbar_init(&M.g2done[b], 1);
-      umma::mbar_init(&M.d2free[b], 128);
     }
-    umma::mbar_init(&M.ssfull, 128);
     umma::mbar_fence_init();
   }
   if (tid < kMaxOrd) M.cy[0][tid] = make_double2(0.0, 0.0);
-  if (warp == 0) umma::tmem_alloc(&M.tmem, 256);
+  if (warp == 0) umma::tmem_alloc(&M.tmem, 512);
   umma::fence_proxy_async();
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, M.tmem, 0);  // warp-uniform
   constexpr int nord = NORD;
+  const uint64_t dbase = umma::desc_sw128(umma::smem_u32(sm));
 
-  if (warp >= 8 && warp < 12) {
-    // ================= loader: complete tile gt-1 (lo tiles, xfull), then stage tile gt
-    // into its buffer once GEMM2 of tile gt-2 has released it, and prefetch tile gt+1's
-    // samples into L2 so its copies hit L2
-    const int lt = tid - 256;
+  if (warp >= 12) {
+    // ================= loader: warp q owns chunk rows [32 q, +32) = TMEM lanes of warp q
+    const int q = warp - 12;
+    const uint32_t lrow = static_cast<uint32_t>(q * 32) << 16;
+    float* const stg = reinterpret_cast<float*>(sm + kLStage + q * kStgWarp);
     unsigned long long keep, first;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(first));
-    Walk w;
+    const uint32_t idm = umma::idesc_tf32(128, NO + 16), ida = umma::idesc_tf32(128, 16);
+    auto issue = [&](const Walk& w, int buf) {
+      if (w.valid) {
+        const float* xs = P.x + w.sig * P.ld_x;
+        const long long lo = P.lo + w.obase, o0 = w.o0(P) + 32LL * kQ * q, jmin = lo - P.K;
+        float* sb = stg + buf * 2 * 32 * kStgRow;
+        stage_rows(P, xs, lo + o0 + P.K, jmin, lane, keep, sb);
+        if (!w.warm(P)) stage_rows(P, xs, lo + o0 - P.K, jmin, lane, first, sb + 32 * kStgRow);
+        if (lane == 0) {
+          Walk nx = w;
+          nx.advance(P);
+          if (nx.valid) {
+            const float* xn = P.x + nx.sig * P.ld_x;
+            const long long ln = P.lo + nx.obase, on = nx.o0(P) + 32LL * kQ * q;
+            prefetch_l2(xn, ln + on + P.K, P.n);
+            if (!nx.warm(P)) prefetch_l2(xn, ln + on - P.K, P.n);
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");  // one group per tile (possibly empty)
+    };
+    // staging ring of kLoadAhead + 1 tiles: tile gt + kLoadAhead is issued before tile gt
+    // is moved into TMEM
+    Walk wi, w;
+    wi.begin(P);
     w.begin(P);
-    bool pend_l = false, pend_t = false;  // previous tile's streams still in flight
-    long long gt = 0;
-    for (; w.valid; ++gt) {
+    for (int k = 0; k < kLoadAhead; ++k) {
+      issue(wi, k);
+      if (wi.valid) wi.advance(P);
+    }
+    for (long long gt = 0; w.valid; ++gt) {
+      issue(wi, static_cast<int>((gt + kLoadAhead) % (kLoadAhead + 1)));
+      if (wi.valid) wi.advance(P);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kLoadAhead) : "memory");
+      __syncwarp();
       const int b = static_cast<int>(gt & 1);
-      if (gt >= 1) {
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        if (lt == 0) trace_ev(P, gt - 1, 14);
-        unsigned char* pb = sm + kX + (b ^ 1) * 4 * kXT;
-        if (pend_l) finish_lo(pb, pb + kXT, lt);
-        if (pend_t) finish_lo(pb + 2 * kXT, pb + 3 * kXT, lt);
-        umma::fence_proxy_async();
-        umma::mbar_arrive(&M.xfull[b ^ 1]);
-        if (lt == 0) trace_ev(P, gt - 1, 1);
-      }
-      Walk nx = w;
-      nx.advance(P);
-      if (lt == 0 && nx.valid) {
-        const float* xs = P.x + nx.sig * P.ld_x;
-        const long long lo = P.lo + nx.obase, o0 = nx.o0(P);
-        prefetch_l2(xs, lo + o0 + P.K, P.n);
-        if (!nx.warm(P)) prefetch_l2(xs, lo + o0 - P.K, P.n);
-      }
       if (gt >= 2) umma::mbar_wait(&M.xfree[b], static_cast<uint32_t>(((gt >> 1) - 1) & 1));
-      if (lt == 0) trace_ev(P, gt, 0);
-      unsigned char* xb = sm + kX + b * 4 * kXT;
-      const float* xs = P.x + w.sig * P.ld_x;
-      const long long lo = P.lo + w.obase, o0 = w.o0(P), jmin = lo - P.K;
-      pend_l = stage_stream(P, xs, lo + o0 + P.K, jmin, lt, keep, xb, xb + kXT);
-      pend_t = !w.warm(P) && stage_stream(P, xs, lo + o0 - P.K, jmin, lt, first, xb + 2 * kXT, xb + 3 * kXT);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      w = nx;
-    }
-    if (gt >= 1) {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      const int b = static_cast<int>((gt - 1) & 1);
-      unsigned char* pb = sm + kX + b * 4 * kXT;
-      if (pend_l) finish_lo(pb, pb + kXT, lt);
-      if (pend_t) finish_lo(pb + 2 * kXT, pb + 3 * kXT, lt);
-      umma::fence_proxy_async();
-      umma::mbar_arrive(&M.xfull[b]);
-    }
-  } else if (warp >= 12) {
-    // ================= MMA issuers (warp-uniform control flow, one elected lane issues):
-    // warp 12 runs GEMM1 of every tile as soon as its samples are staged; warp 13 runs
-    // GEMM2 of every output tile as soon as its chunk states are. All operand addresses
-    // are compile-time offsets from one descriptor base per (stage, accumulator buffer).
-    const uint64_t dbase = umma::desc_sw128(umma::smem_u32(sm));
-    Walk w;
-    w.begin(P);
-    if (warp == 12) {
-      for (long long g = 0; w.valid; ++g, w.advance(P)) {
-        const int b = static_cast<int>(g & 1);
-        umma::mbar_wait(&M.xfull[b], static_cast<uint32_t>((g >> 1) & 1));
-        if (g >= 2) umma::mbar_wait(&M.d1free[b], static_cast<uint32_t>(((g >> 1) - 1) & 1));
+      __syncwarp();
+      umma::fence_after();
+      if (lane == 0) trace_ev(P, gt, 0);
+      const float* sb = stg + static_cast<int>(gt % (kLoadAhead + 1)) * 2 * 32 * kStgRow;
+      const uint32_t tx = tmem + lrow + kTX + 128 * b;
+      const bool warm = w.warm(P);
+      row_to_tmem(sb, lane, tx);
+      if (!warm) row_to_tmem(sb + 32 * kStgRow, lane, tx + 64);
+      umma::tmem_wait_st();
+      umma::fence_before();
+      bar_named(4, 128);  // all four lane quarters of the tile are in TMEM
+      if (lane == 0) trace_ev(P, gt, 1);
+      if (q == 0) {
+        // merged GEMM (outputs + aggregates; warm tiles: aggregates of the lead stream)
+        // into accumulator b once the epilogue / scan have released it
+        if (gt >= 2) umma::mbar_wait(&M.dfree[b], static_cast<uint32_t>(((gt >> 1) - 1) & 1));
         __syncwarp();
         umma::fence_after();
-        const bool trail = !w.warm(P);
-        if (b == 0)
-          gemm1<0>(dbase, tmem, trail);
-        else
-          gemm1<1>(dbase, tmem, trail);
+        const uint32_t d = tmem + (b ? kTD1 : kTD0), x = tmem + kTX + 128 * b;
+        if (!warm) {
+          merged_k<0>(dbase, d, x, idm);
+          merged_k<1>(dbase, d, x, idm);
+          merged_k<2>(dbase, d, x, idm);
+          merged_k<3>(dbase, d, x, idm);
+        } else if (NO == 64) {
+          warm_k<0, 64>(dbase, d + 64, x, ida);
+          warm_k<1, 64>(dbase, d + 64, x, ida);
+          warm_k<2, 64>(dbase, d + 64, x, ida);
+          warm_k<3, 64>(dbase, d + 64, x, ida);
+        } else {
+          warm_k<0, 32>(dbase, d + 32, x, ida);
+          warm_k<1, 32>(dbase, d + 32, x, ida);
+          warm_k<2, 32>(dbase, d + 32, x, ida);
+          warm_k<3, 32>(dbase, d + 32, x, ida);
+        }
         umma::commit_elect(&M.g1done[b]);
-        if (!trail) umma::commit_elect(&M.xfree[b]);
-        if (lane == 0) trace_ev(P, g, 2);
+        umma::commit_elect(&M.xfree[b]);
+        if (lane == 0) trace_ev(P, gt, 2);
       }
-    } else {
-      long long u = 0;
-      for (long long g = 0; w.valid; ++g, w.advance(P)) {
-        if (w.warm(P)) continue;
-        const int b2 = static_cast<int>(u & 1);
-        umma::mbar_wait(&M.ssfull, static_cast<uint32_t>(u & 1));
-        if (lane == 0) trace_ev(P, g, 15);
-        if (u >= 2) umma::mbar_wait(&M.d2free[b2], static_cast<uint32_t>(((u >> 1) - 1) & 1));
-        __syncwarp();
-        umma::fence_after();
-        const int sel = static_cast<int>(g & 1) * 2 + b2;
-        if (sel == 0)
-          gemm2<0, 0>(dbase, tmem, P.cplx);
-        else if (sel == 1)
-          gemm2<0, 1>(dbase, tmem, P.cplx);
-        else if (sel == 2)
-          gemm2<1, 0>(dbase, tmem, P.cplx);
-        else
-          gemm2<1, 1>(dbase, tmem, P.cplx);
-        umma::commit_elect(&M.g2done[b2]);
-        umma::commit_elect(&M.xfree[g & 1]);
-        if (lane == 0) trace_ev(P, g, 5);
-        ++u;
-      }
+      __syncwarp();  // every lane has read its row before the ring slot is refilled
+      w.advance(P);
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 8) {
     // ================= epilogue (non-warm tiles): thread = chunk = TMEM lane
-    const int c = tid - 128;
-    const uint32_t lrow = static_cast<uint32_t>((warp - 4) * 32) << 16;
-    unsigned char* const stg = sm + kStage;
-    const int ew = warp - 4;
+    const int c = tid - 256;
+    const int ew = warp - 8;
+    const uint32_t lrow = static_cast<uint32_t>(ew * 32) << 16;
+    unsigned char* const stgo = sm + kStage;
     const int halves = P.cplx ? 2 : 1;
     const int cw = P.cplx ? 2 : 1;
     Walk w;
     w.begin(P);
-    long long u = 0, gt = -1;
-    for (; w.valid; w.advance(P)) {
-      ++gt;
+    long long u = 0;
+    for (long long gt = 0; w.valid; w.advance(P), ++gt) {
       if (w.warm(P)) continue;
-      const int b2 = static_cast<int>(u & 1);
-      umma::mbar_wait(&M.g2done[b2], static_cast<uint32_t>((u >> 1) & 1));
+      const int s = static_cast<int>(u & 1);
+      umma::mbar_wait(&M.g2done[s], static_cast<uint32_t>((u >> 1) & 1));
       if (c == 0) trace_ev(P, gt, 6);
       __syncwarp();
       umma::fence_after();
-      uint32_t v[64];
-      if (halves == 2) {
-        umma::tmem_ld32(tmem + lrow + 64 * b2, v);
-        umma::tmem_ld32(tmem + lrow + 64 * b2 + 32, v + 32);
-      } else {
-        umma::tmem_ld32(tmem + lrow + 64 * b2, v);
+      const uint32_t dcol = (gt & 1) ? kTD1 : kTD0;
+      // accumulator -> staging (row c: 8 chunks of 16 B per half, chunk q at q ^ (c & 7))
+      for (int h = 0; h < halves; ++h) {
+        uint32_t v[32];
+        umma::tmem_ld32(tmem + lrow + dcol + 32 * h, v);
+        umma::tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<uint4*>(stgo + h * 16384 + c * 128 + ((q ^ (c & 7)) << 4)) =
+              make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       }
-      umma::tmem_wait_ld();
       umma::fence_before();
-      umma::mbar_arrive(&M.d2free[b2]);
+      umma::mbar_arrive(&M.dfree[gt & 1]);
+      if (c == 0) trace_ev(P, gt, 14);
       ++u;
+      bar_named(3, 128);
       const long long o0 = w.o0(P), cnt = w.cnt;
       float* const orow = P.out + (w.sig * P.ld_out + w.obase) * cw;
+      for (int h = 0; h < halves; ++h) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (h < halves) {
-          // row c of the staging area: 8 chunks of 16 B, chunk q at q ^ (c & 7)
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            *reinterpret_cast<uint4*>(stg + c * 128 + ((q ^ (c & 7)) << 4)) =
-                make_uint4(v[32 * h + 4 * q], v[32 * h + 4 * q + 1], v[32 * h + 4 * q + 2], v[32 * h + 4 * q + 3]);
-          bar_epi();
-#pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            const int row = ew * 32 + r * 4 + (lane >> 3), q = lane & 7;
-            const float4 val = *reinterpret_cast<const float4*>(stg + row * 128 + ((q ^ (row & 7)) << 4));
-            const long long pos = o0 + row * 32 + (P.cplx ? 16 * h + 2 * q : 4 * q);
-            float* dst = orow + (o0 + row * 32) * cw + 32 * h + 4 * q;
-            const int per = P.cplx ? 2 : 4;
-            if (P.vec_ok && pos + per <= cnt) {
-              __stcs(reinterpret_cast<float4*>(dst), val);
-            } else {
-              const float e[4] = {val.x, val.y, val.z, val.w};
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                if (pos + j / cw < cnt) dst[j] = e[j];
-            }
-          }
-          bar_epi();
+        for (int r = 0; r < 8; ++r) {
+          const int row = ew * 32 + r * 4 + (lane >> 3), q = lane & 7;
+          const float4 val = *reinterpret_cast<const float4*>(stgo + h * 16384 + row * 128 + ((q ^ (row & 7)) << 4));
+          const long long pos = o0 + row * 32 + (P.cplx ? 16 * h + 2 * q : 4 * q);
+          float* dst = orow + (o0 + row * 32) * cw + 32 * h + 4 * q;
+          if (P.vec_ok && pos + (P.cplx ? 2 : 4) <= cnt)
+            __stcs(reinterpret_cast<float4*>(dst), val);
+          else
+            store_masked(dst, val, pos, cnt, cw);
         }
       }
+      bar_named(3, 128);  // staging reusable
       if (c == 0) trace_ev(P, gt, 7);
     }
   } else {
-    // ================= chunk-state scan: thread = chunk = TMEM lane
+    // ================= chunk-state scan: thread = chunk = TMEM lane; order set `os`
+    constexpr int hA = 4;  // set 0: orders [0, 4) (state columns 0-7), set 1: [4, 8) (8-15)
+    const int os = warp >> 2;
+    const int sw = warp & 3;   // lane quarter
+    const int p0 = os ? hA : 0;
+    const int st = tid & 127;
     const float2* zl = reinterpret_cast<const float2*>(sm + kZl);
-    const uint32_t lrow = static_cast<uint32_t>(warp * 32) << 16;
-    unsigned char* const ss = sm + kSS;
-    const int c = tid;
+    const uint32_t lrow = static_cast<uint32_t>(sw * 32) << 16;
     Walk w;
     w.begin(P);
     long long u = 0;
@@ -422,105 +386,128 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       const int b = static_cast<int>(gt & 1);
       umma::mbar_wait(&M.g1done[b], static_cast<uint32_t>((gt >> 1) & 1));
       if (tid == 0) trace_ev(P, gt, 3);
-      if (tid == 96) trace_ev(P, gt, 8);
       __syncwarp();
       umma::fence_after();
-      uint32_t a16[16];
-      umma::tmem_ld16(tmem + lrow + 128 + 32 * b, a16);
-      umma::tmem_wait_ld();
-      umma::fence_before();
-      umma::mbar_arrive(&M.d1free[b]);
       const bool warm = w.warm(P);
-      float2 inc[kMaxOrd];
+      uint32_t a8[8];
+      umma::tmem_ld8(tmem + lrow + (b ? kTD1 : kTD0) + NO + 2 * p0, a8);  // this set's orders
+      umma::tmem_wait_ld();
+      if (tid == 0) trace_ev(P, gt, 8);
+      if (warm) {
+        // nothing else reads this accumulator: hand it back once both sets have read it
+        umma::fence_before();
+        bar_named(5, 256);
+        if (warp == 0) {
+          __syncwarp();
+          if (lane == 0) umma::mbar_arrive_cnt(&M.dfree[b], 128);
+        }
+      }
+      float2 inc[4];
       if (warm) {
         // only the tile total is needed: sum_l z^{32 (31 - l)} A[l] per warp
 #pragma unroll
-        for (int p = 0; p < kMaxOrd; ++p) {
-          if (p < nord) {
-            const float2 a = make_float2(__uint_as_float(a16[2 * p]), __uint_as_float(a16[2 * p + 1]));
+        for (int j = 0; j < 4; ++j) {
+          const int p = p0 + j;
+          if (j < hA && p < nord) {
+            const float2 a = make_float2(__uint_as_float(a8[2 * j]), __uint_as_float(a8[2 * j + 1]));
             float2 s = cmla(zl[p * 32 + 31 - lane], a, make_float2(0.f, 0.f));
 #pragma unroll
             for (int d = 16; d >= 1; d >>= 1) {
               s.x += __shfl_xor_sync(0xffffffffu, s.x, d);
               s.y += __shfl_xor_sync(0xffffffffu, s.y, d);
             }
-            if (lane == 0) M.wtot[b][warp][p] = s;
+            if (lane == 0) M.wtot[b][sw][p] = s;
           }
         }
       } else {
         // inclusive warp scan over chunks: I[l] = sum_{l' <= l} z^{32 (l - l')} A[l']
-        // (steps outer, orders inner: the orders' shuffle chains overlap)
 #pragma unroll
-        for (int p = 0; p < kMaxOrd; ++p)
-          if (p < nord) inc[p] = make_float2(__uint_as_float(a16[2 * p]), __uint_as_float(a16[2 * p + 1]));
+        for (int j = 0; j < 4; ++j) inc[j] = make_float2(__uint_as_float(a8[2 * j]), __uint_as_float(a8[2 * j + 1]));
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
           const int d = 1 << k;
-          float2 t[kMaxOrd];
+          float2 t[4];
 #pragma unroll
-          for (int p = 0; p < kMaxOrd; ++p)
-            if (p < nord)
-              t[p] = make_float2(__shfl_up_sync(0xffffffffu, inc[p].x, d), __shfl_up_sync(0xffffffffu, inc[p].y, d));
+          for (int j = 0; j < 4; ++j)
+            if (j < hA && p0 + j < nord)
+              t[j] = make_float2(__shfl_up_sync(0xffffffffu, inc[j].x, d), __shfl_up_sync(0xffffffffu, inc[j].y, d));
 #pragma unroll
-          for (int p = 0; p < kMaxOrd; ++p)
-            if (p < nord && lane >= d) inc[p] = cmla(P.zs[p][k], t[p], inc[p]);
+          for (int j = 0; j < 4; ++j)
+            if (j < hA && p0 + j < nord && lane >= d) inc[j] = cmla(P.zs[p0 + j][k], t[j], inc[j]);
         }
         if (lane == 31) {
 #pragma unroll
-          for (int p = 0; p < kMaxOrd; ++p)
-            if (p < nord) M.wtot[b][warp][p] = inc[p];
+          for (int j = 0; j < 4; ++j)
+            if (j < hA && p0 + j < nord) M.wtot[b][sw][p0 + j] = inc[j];
         }
       }
       if (tid == 0) trace_ev(P, gt, 9);
-      if (tid == 96) trace_ev(P, gt, 10);
-      bar_scan();
+      bar_named(1 + os, 128);
       if (tid == 0) trace_ev(P, gt, 11);
       const double2* cyin = M.cy[b];
       if (!warm) {
-        // state entering chunk c: S = excl + z^{32 lane} W_warp. Lane p < nord derives
-        // W_warp for order p from the fp64 tile carry and the earlier warps' totals.
+        // state entering chunk c: S = excl + z^{32 lane} W_warp. Lane j < set size derives
+        // W_warp for order p0 + j from the fp64 tile carry and the earlier warps' totals.
         float2 Wp = make_float2(0.f, 0.f);
-        if (lane < nord) {
-          const double2 z = P.z1024[lane];
-          double2 Wd = cyin[lane];
-          for (int w2 = 0; w2 < warp; ++w2) {
-            const float2 t = M.wtot[b][w2][lane];
+        if (lane < hA && p0 + lane < nord) {
+          const int p = p0 + lane;
+          const double2 z = P.z1024[p];
+          double2 Wd = cyin[p];
+          for (int w2 = 0; w2 < sw; ++w2) {
+            const float2 t = M.wtot[b][w2][p];
             Wd = make_double2(fma(z.x, Wd.x, fma(-z.y, Wd.y, static_cast<double>(t.x))),
                               fma(z.x, Wd.y, fma(z.y, Wd.x, static_cast<double>(t.y))));
           }
           Wp = make_float2(static_cast<float>(Wd.x), static_cast<float>(Wd.y));
         }
-        float sv[2 * kMaxOrd];
+        uint32_t sh[8], sl[8];
 #pragma unroll
-        for (int p = 0; p < kMaxOrd; ++p) {
+        for (int j = 0; j < 4; ++j) {
           float2 s = make_float2(0.f, 0.f);
-          if (p < nord) {
-            const float2 W = make_float2(__shfl_sync(0xffffffffu, Wp.x, p), __shfl_sync(0xffffffffu, Wp.y, p));
-            float2 e = make_float2(__shfl_up_sync(0xffffffffu, inc[p].x, 1), __shfl_up_sync(0xffffffffu, inc[p].y, 1));
+          if (j < hA && p0 + j < nord) {
+            const float2 W = make_float2(__shfl_sync(0xffffffffu, Wp.x, j), __shfl_sync(0xffffffffu, Wp.y, j));
+            float2 e = make_float2(__shfl_up_sync(0xffffffffu, inc[j].x, 1), __shfl_up_sync(0xffffffffu, inc[j].y, 1));
             if (lane == 0) e = make_float2(0.f, 0.f);
-            s = cmla(zl[p * 32 + lane], W, e);
+            s = cmla(zl[(p0 + j) * 32 + lane], W, e);
           }
-          sv[2 * p] = s.x;
-          sv[2 * p + 1] = s.y;
+          // head = the raw value (the MMA reads its TF32 head), remainder separately
+          sh[2 * j] = __float_as_uint(s.x);
+          sh[2 * j + 1] = __float_as_uint(s.y);
+          sl[2 * j] = __float_as_uint(tf32_lo(s.x));
+          sl[2 * j + 1] = __float_as_uint(tf32_lo(s.y));
         }
-        // the chunk-state operand is free once GEMM2 of the previous tile is done
-        if (u >= 1) umma::mbar_wait(&M.g2done[(u - 1) & 1], static_cast<uint32_t>(((u - 1) >> 1) & 1));
         if (tid == 0) trace_ev(P, gt, 12);
-        // hi = the raw value (the MMA reads its TF32 head), lo = the remainder
-#pragma unroll
-        for (int k = 0; k < 2 * kMaxOrd; ++k) {
-          *reinterpret_cast<float*>(ss + umma::sw128_off(c, k)) = sv[k];
-          *reinterpret_cast<float*>(ss + umma::sw128_off(c, 16 + k)) = tf32_lo(sv[k]);
-        }
-        umma::fence_proxy_async();
-        umma::mbar_arrive(&M.ssfull);
+        // this state buffer is free once the chunk-state GEMM of output tile u-2 is done
+        const int s = static_cast<int>(u & 1);
+        if (u >= 2) umma::mbar_wait(&M.g2done[s], static_cast<uint32_t>(((u >> 1) - 1) & 1));
+        __syncwarp();
+        umma::fence_after();
+        const uint32_t ts = tmem + lrow + kTSS + 32 * s + 2 * p0;
+        umma::tmem_st8(ts, sh);
+        umma::tmem_st8(ts + 16, sl);
+        umma::tmem_wait_st();
+        umma::fence_before();
+        bar_named(5, 256);  // both order sets' states are in TMEM
         if (tid == 0) trace_ev(P, gt, 4);
-        if (tid == 96) trace_ev(P, gt, 13);
+        if (warp == 0) {
+          // chunk-state GEMM: D[:, 0:NO) += S . C^T (3xTF32)
+          umma::fence_after();
+          const uint32_t d = tmem + (b ? kTD1 : kTD0), a = tmem + kTSS + 32 * s;
+          const uint32_t ids = umma::idesc_tf32(128, NO);
+          umma::mma_tf32_ts<kBC>(d, a, dbase, ids, 1);  // S_h . C_h
+          umma::mma_tf32_ts<kBC + 32>(d, a + 8, dbase, ids, 1);
+          umma::mma_tf32_ts<kBC>(d, a + 16, dbase, ids, 1);  // S_l . C_h
+          umma::mma_tf32_ts<kBC + 32>(d, a + 24, dbase, ids, 1);
+          umma::mma_tf32_ts<kBC + 64>(d, a, dbase, ids, 1);  // S_h . C_l
+          umma::mma_tf32_ts<kBC + 96>(d, a + 8, dbase, ids, 1);
+          umma::commit_elect(&M.g2done[s]);
+          if (lane == 0) trace_ev(P, gt, 5);
+        }
         ++u;
       }
-      if (tid < nord) {
+      if (st < hA && p0 + st < nord && sw == 0) {
         // carry into the next tile (fp64): z^{4096} C + sum_w z^{1024 (3 - w)} T_w
-        const int p = tid;
+        const int p = p0 + st;
         const double2 z = P.z1024[p], zt = P.zT[p];
         double2 T = make_double2(0.0, 0.0);
         for (int w2 = 0; w2 < 4; ++w2) {
@@ -541,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
   __syncthreads();
   if (warp == 0) {
     umma::fence_after();
-    umma::tmem_free(tmem, 256);
+    umma::tmem_free(tmem, 512);
   }
 }
 

@@ -11,20 +11,26 @@ namespace tck {
 constexpr int kQ = 32;           // positions per chunk (GEMM K per stream)
 constexpr int kNC = 128;         // chunks per tile (GEMM M)
 constexpr int kTile = kQ * kNC;  // 4096 positions
-constexpr int kMaxOrd = 8;       // 2 * orders <= 16 = GEMM1 N
-constexpr int kThreads = 448;  // 14 warps: scan, epilogue, loader, 2 MMA issuers
+constexpr int kMaxOrd = 8;       // 2 * orders <= 16 aggregate columns
+constexpr int kThreads = 512;    // 16 warps: scan (2 order sets), epilogue, loader
 
-// shared-memory image (bytes; SW128 regions 1024-aligned)
-constexpr uint32_t kHLh = 0, kHLl = 8192, kHTh = 16384, kHTl = 24576, kBC1 = 32768, kBC2 = 40960;
-constexpr uint32_t kALh = 49152, kALl = 51200, kATh = 53248, kATl = 55296;
-constexpr uint32_t kZl = 57344;        // float2 [kMaxOrd][32]: z^{32 l}
-constexpr uint32_t kImage = 59392;     // bytes copied from the plan's device image
-constexpr uint32_t kX = kImage;        // [2 stages][XLh, XLl, XTh, XTl] x 16 KB
-constexpr uint32_t kXT = 16384;
-constexpr uint32_t kSS = kX + 2 * 4 * kXT;  // chunk-state operand [S_hi | S_lo]
-constexpr uint32_t kStage = kSS + kXT;      // epilogue staging (128 rows x 128 B)
-constexpr uint32_t kMisc = kStage + kXT;
+// shared-memory image (bytes; SW128 K-major B operands, 1024-aligned regions).
+// BL/BT: [output rows (NO = 64 complex / 32 real) ; 16 aggregate rows] x 32 positions for
+// the lead / trail streams, TF32 head (h) and remainder (l); BC: chunk-state -> output,
+// columns [C head (16) | C remainder (16)].
+constexpr uint32_t kBLh = 0, kBLl = 10240, kBTh = 20480, kBTl = 30720, kBC = 40960;
+constexpr uint32_t kZl = 49152;     // float2 [kMaxOrd][32]: z^{32 l}
+constexpr uint32_t kImage = 51200;  // bytes copied from the plan's device image
+constexpr uint32_t kStgRow = 36;    // padded staging row (floats): conflict-free row reads
+constexpr int kLoadAhead = 2;       // loader lookahead (tiles in flight ahead of the one stored)
+constexpr uint32_t kStgWarp = (kLoadAhead + 1) * 2 * 32 * kStgRow * 4;  // [ring slot][stream][32 rows]
+constexpr uint32_t kLStage = kImage;                     // loader staging, 4 warps
+constexpr uint32_t kStage = kLStage + 4 * kStgWarp;      // epilogue staging (128 rows x 128 B)
+constexpr uint32_t kMisc = kStage + 32768;  // epilogue staging: two halves
 constexpr uint32_t kSmemBytes = kMisc + 1024 + 1024;  // misc + alignment slack
+// TMEM columns (512 allocated): X operands [stage][xl_h, xl_l, xt_h, xt_l] x 32,
+// chunk states [2][S_h (16) | S_l (16)], accumulators [2][outputs | aggregates]
+constexpr uint32_t kTX = 0, kTSS = 256, kTD0 = 320, kTD1 = 416;
 
 struct TcParams {
   const float* x;

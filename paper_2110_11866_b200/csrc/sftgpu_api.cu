@@ -520,15 +520,16 @@ bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
     ht[d] = st;
   }
   const int comps = cplx ? 2 : 1;
+  const int NO = comps * tck::kQ;  // output rows of the merged B operands; aggregates follow
   for (int i = 0; i < tck::kQ; ++i)
     for (int r = 0; r < comps; ++r) {
       const int j = comps * i + r;
       for (int m = 0; m <= i; ++m) {
         const cd vl = hl[i - m], vt = ht[i - m];
-        put_split(tck::kHLh, tck::kHLl, j, m, r == 0 ? vl.real() : vl.imag());
-        put_split(tck::kHTh, tck::kHTl, j, m, r == 0 ? vt.real() : vt.imag());
+        put_split(tck::kBLh, tck::kBLl, j, m, r == 0 ? vl.real() : vl.imag());
+        put_split(tck::kBTh, tck::kBTl, j, m, r == 0 ? vt.real() : vt.imag());
       }
-      // chunk start state S_p -> output i: K_p(z^{i+1} S_p)
+      // chunk start state S_p -> output i: K_p(z^{i+1} S_p); columns [head | remainder]
       for (int p = 0; p < nord; ++p) {
         const cd a = zpow(alpha, ords[p].omega, i + 1.0);
         const double k0 = r == 0 ? kw[p][0] : kw[p][2], k1 = r == 0 ? kw[p][1] : kw[p][3];
@@ -536,20 +537,19 @@ bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
         for (int q = 0; q < 2; ++q) {
           const double v = q == 0 ? cr : ci;
           const float h = tf32_head(static_cast<float>(v));
-          put(tck::kBC1, j, 2 * p + q, h);
-          put(tck::kBC1, j, 16 + 2 * p + q, h);
-          put(tck::kBC2, j, 2 * p + q, static_cast<float>(v - static_cast<double>(h)));
+          put(tck::kBC, j, 2 * p + q, h);
+          put(tck::kBC, j, 16 + 2 * p + q, static_cast<float>(v - static_cast<double>(h)));
         }
       }
     }
-  // chunk aggregates A_p = sum_m z^{31-m} (xl[m] - c xt[m])
+  // chunk aggregates A_p = sum_m z^{31-m} (xl[m] - c xt[m]) in rows NO + 2p (+1)
   for (int p = 0; p < nord; ++p)
     for (int m = 0; m < tck::kQ; ++m) {
       const cd zl = zpow(alpha, ords[p].omega, tck::kQ - 1.0 - m), zt = -cinj * zl;
-      put_split(tck::kALh, tck::kALl, 2 * p, m, zl.real());
-      put_split(tck::kALh, tck::kALl, 2 * p + 1, m, zl.imag());
-      put_split(tck::kATh, tck::kATl, 2 * p, m, zt.real());
-      put_split(tck::kATh, tck::kATl, 2 * p + 1, m, zt.imag());
+      put_split(tck::kBLh, tck::kBLl, NO + 2 * p, m, zl.real());
+      put_split(tck::kBLh, tck::kBLl, NO + 2 * p + 1, m, zl.imag());
+      put_split(tck::kBTh, tck::kBTl, NO + 2 * p, m, zt.real());
+      put_split(tck::kBTh, tck::kBTl, NO + 2 * p + 1, m, zt.imag());
     }
   tck::TcParams& P = pl->tcp;
   std::memset(&P, 0, sizeof(P));
