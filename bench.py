@@ -6,7 +6,7 @@ Default workload = BASELINE.json's headline: the Morlet wavelet transform, metho
 one signal. ``--workload`` selects the other BASELINE configs (1, 2, 4, 5).
 
 Arms:
-  --impl ours (default)   the product: libsftgpu K1 kernel through the C ABI.
+  --impl ours (default)   the product: libsftgpu (K4 tensor-core / K1 scan kernels) through the C ABI.
   --impl reference        the reference's CPU path (restated in oracle/, the reference
                           itself does not build here: no Eigen3) on all host threads.
 Multi-GPU: one process per GPU (torchrun); single-signal workloads run independent
@@ -161,6 +161,13 @@ def measured_peaks():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:  # noqa: BLE001
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def kernel_name(plan) -> str:
+    """The dominant kernel of a plan: K4 (tensor cores) or K1 (CUDA-core scan)."""
+    if plan.describe().get("tensor_cores"):
+        return "sft_tc_kernel (K4: tcgen05 kind::tf32 3xTF32 chunked scan)"
+    return "sft_scan_kernel (K1)"
 
 
 def ncu_traffic(workload: str):
@@ -373,7 +380,7 @@ def run_ours(args, w, spec_of):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": step_bytes / launches,
-                         "kernel": "sft_scan_kernel (K1)", "kernel_ms": kernel_ms},
+                         "kernel": kernel_name(plan), "kernel_ms": kernel_ms},
             "e2e": {"value": e2e_value, "unit": "Msamples·scales/s", "h2d_bytes_per_step": batch * n * in_es,
                     "d2h_bytes_per_step": batch * n * out_es, "steps": e2e_steps,
                     "path": e2e_path},
@@ -470,7 +477,8 @@ def run_scalogram(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": ncu_traffic("scalogram"), "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": step_bytes / max(1, launches_per_step),
-                         "kernel": "sft_scan_kernel (K1), one launch per scale", "kernel_ms": kernel_ms},
+                         "kernel": kernel_name(sc.plans[0]) + ", one launch per scale" if sc.plans
+                         else "none", "kernel_ms": kernel_ms},
             "e2e": {"value": e2e_value, "unit": "Msamples·scales/s", "h2d_bytes_per_step": n * 4,
                     "d2h_bytes_per_step": sc.output_bytes(), "steps": 1,
                     "path": "Scalogram.run (public API) with pinned host input/output"},

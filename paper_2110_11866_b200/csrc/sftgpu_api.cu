@@ -475,9 +475,9 @@ bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
   else
     return no("orders do not share one injection constant");
   if (!force) {
-    // auto-selection only once K4 beats K1 on the batched shapes (SFTGPU_TC=1 opts in)
-    const char* env = std::getenv("SFTGPU_TC");
-    if (!env || env[0] != '1') return false;
+    // auto: K4 once the transform spans >= 4 tiles per SM (SFTGPU_NO_TC=1 keeps K1)
+    const char* env = std::getenv("SFTGPU_NO_TC");
+    if (env && env[0] == '1') return false;
     const long long tiles = pl->batch * ((pl->count + tck::kTile - 1) / tck::kTile);
     if (tiles < 4LL * 148) return false;
   }

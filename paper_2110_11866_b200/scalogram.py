@@ -82,7 +82,7 @@ class Scalogram:
     """Rank-local part of a scalogram: ``rows`` scales x ``count`` outputs (complex)."""
 
     def __init__(self, n: int, specs, world: int = 1, rank: int = 0, shard: str = "scale",
-                 boundary=S.BoundaryPolicy.Clamp, executor=None, streams: int = 8):
+                 boundary=S.BoundaryPolicy.Clamp, executor=None, streams: int = 8, mode: str = "auto"):
         if shard not in ("scale", "chunk"):
             raise ValueError("shard must be 'scale' or 'chunk'")
         self.n, self.specs, self.world, self.rank, self.shard = n, list(specs), world, rank, shard
@@ -98,10 +98,14 @@ class Scalogram:
         self.n_streams = streams
         self._streams = None
         if executor is None:
-            # sequential (chunked) plans: scales run concurrently on several streams, so
-            # each plan needs only a few CTAs and no inter-CTA look-back
-            self.plans = [S.TransformPlan(self.specs[i], n, 1, boundary, (self.begin, self.count), mode="seq")
-                          for i in self.rows]
+            # mode "auto": K4 (tensor cores, one persistent CTA per SM per scale) where the
+            # scale qualifies, else sequential K1 plans (chunked, few CTAs each, so scales
+            # run concurrently on several streams with no inter-CTA look-back)
+            for i in self.rows:
+                p = S.TransformPlan(self.specs[i], n, 1, boundary, (self.begin, self.count), mode=mode)
+                if mode == "auto" and not p.describe()["tensor_cores"]:
+                    p = S.TransformPlan(self.specs[i], n, 1, boundary, (self.begin, self.count), mode="seq")
+                self.plans.append(p)
 
     @property
     def launches(self) -> int:

@@ -76,9 +76,12 @@ def test_tc_ranged_plan_matches_full(sft, O):
 
 
 def test_tc_selection(sft, O):
+    """Auto mode picks K4 for eligible transforms spanning >= 4 x 148 tiles (config 4)."""
     spec = sft.make_transform_spec("MMS5P3", 8192.0, 10.0, sft.TransformOptions(precision=0))
-    assert sft.TransformPlan(spec, 102400, 4096, mode="tc").describe()["tensor_cores"] == 1
+    assert sft.TransformPlan(spec, 102400, 4096).describe()["tensor_cores"] == 1
     assert sft.TransformPlan(spec, 102400, 1).describe()["tensor_cores"] == 0
+    fp64 = sft.make_transform_spec("MMS5P3", 8192.0, 10.0, sft.TransformOptions(precision=1))
+    assert sft.TransformPlan(fp64, 102400, 4096).describe()["tensor_cores"] == 0
 
 
 def test_tc_rejects_ineligible_specs(sft):
