@@ -337,7 +337,11 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       __syncwarp();
       umma::fence_after();
       const uint32_t dcol = (gt & 1) ? kTD1 : kTD0;
-      // accumulator -> staging (row c: 8 chunks of 16 B per half, chunk q at q ^ (c & 7))
+      // the previous tile's TMA stores must have read the staging area
+      if (c == 0 && P.use_tma) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      bar_named(3, 128);
+      // accumulator -> staging (row c: 8 chunks of 16 B per half, chunk q at q ^ (c & 7):
+      // the TMA SWIZZLE_128B layout of a [128 rows][32 floats] box)
       for (int h = 0; h < halves; ++h) {
         uint32_t v[32];
         umma::tmem_ld32(tmem + lrow + dcol + 32 * h, v);
@@ -351,8 +355,33 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       umma::mbar_arrive(&M.dfree[gt & 1]);
       if (c == 0) trace_ev(P, gt, 14);
       ++u;
-      bar_named(3, 128);
       const long long o0 = w.o0(P), cnt = w.cnt;
+      if (P.use_tma) {
+        // one thread hands the tile to the TMA engine: 128 rows x 32 floats per half
+        umma::fence_proxy_async();
+        bar_named(3, 128);
+        if (c == 0) {
+          const int row0 = static_cast<int>((w.obase + o0) / kQ), sg = static_cast<int>(w.sig);
+          for (int h = 0; h < halves; ++h) {
+            const uint32_t src = umma::smem_u32(stgo + h * 16384);
+            if (P.cplx)
+              asm volatile(
+                  "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                      reinterpret_cast<uint64_t>(&P.out_map)),
+                  "r"(0), "r"(h), "r"(row0), "r"(sg), "r"(src)
+                  : "memory");
+            else
+              asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                               reinterpret_cast<uint64_t>(&P.out_map)),
+                           "r"(0), "r"(row0), "r"(sg), "r"(src)
+                           : "memory");
+          }
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (c == 0) trace_ev(P, gt, 7);
+        continue;
+      }
+      bar_named(3, 128);
       float* const orow = P.out + (w.sig * P.ld_out + w.obase) * cw;
       for (int h = 0; h < halves; ++h) {
 #pragma unroll
@@ -367,9 +396,9 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
             store_masked(dst, val, pos, cnt, cw);
         }
       }
-      bar_named(3, 128);  // staging reusable
       if (c == 0) trace_ev(P, gt, 7);
     }
+    if (c == 0 && P.use_tma) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else {
     // ================= chunk-state scan: thread = chunk = TMEM lane; order set `os`
     constexpr int hA = 4;  // set 0: orders [0, 4) (state columns 0-7), set 1: [4, 8) (8-15)

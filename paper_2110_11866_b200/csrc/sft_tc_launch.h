@@ -2,6 +2,7 @@
 // layout constants shared by the plan builder (sftgpu_api.cu) and the kernel.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -33,12 +34,13 @@ constexpr uint32_t kSmemBytes = kMisc + 1024 + 1024;  // misc + alignment slack
 constexpr uint32_t kTX = 0, kTSS = 256, kTD0 = 320, kTD1 = 416;
 
 struct TcParams {
+  CUtensorMap out_map;  // TMA view of the output (see run_tc); valid when use_tma
   const float* x;
   float* out;
   long long n, ld_x, ld_out;  // ld_out in outputs (complex outputs count once)
   long long lo, count;        // first output position, outputs per signal
   long long chunk_len, n_chunks, n_items, warm_tiles;
-  int K, boundary, nord, cplx, vec_ok;
+  int K, boundary, nord, cplx, vec_ok, use_tma;
   const uint4* image;  // kImage bytes
   long long* trace;    // optional: per-tile event clocks of CTA 0 ([64][8]), tools/tc_trace.py
   float2 zs[kMaxOrd][6];  // z^{32 * 2^k} (k < 5), z^{1024}

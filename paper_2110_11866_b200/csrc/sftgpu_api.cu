@@ -132,6 +132,8 @@ struct sftgpu_plan {
   void* d_tc_image = nullptr;
   tck::TcParams tcp{};
   int tc_grid = 0;
+  const void* tc_map_out = nullptr;  // output buffer the cached TMA map describes
+  long long tc_map_ld = -1;
   // pipelined host execution: internal copy-in / compute / copy-out streams and a ring
   // of staging slots, so the transfers of neighbouring calls overlap this call's kernel
   struct Slot {
@@ -838,16 +840,68 @@ sftb::Spec spec_from_c(const sftgpu_spec* o) {
   return s;
 }
 
+// TMA view of the transform output for K4's epilogue: complex [batch][rows][2 halves][32
+// floats], real [batch][rows][32 floats], rows = 32-position chunks. Requires whole
+// chunks per signal (count % 32 == 0) and 16-byte aligned rows; otherwise K4 stores with
+// regular 16-byte stores.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+bool make_out_map(sftgpu_plan* pl, void* out, long long ld_out, CUtensorMap* map) {
+  const tck::TcParams& P = pl->tcp;
+  const int cw = P.cplx ? 2 : 1;
+  if (pl->count % tck::kQ != 0 || reinterpret_cast<uintptr_t>(out) % 16 != 0) return false;
+  if ((static_cast<unsigned long long>(ld_out) * cw * sizeof(float)) % 16 != 0) return false;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  const cuuint64_t rows = static_cast<cuuint64_t>(pl->count / tck::kQ);
+  const cuuint64_t sig_stride = static_cast<cuuint64_t>(ld_out) * cw * sizeof(float);
+  CUresult r;
+  if (cw == 2) {
+    const cuuint64_t dims[4] = {32, 2, rows, static_cast<cuuint64_t>(pl->batch)};
+    const cuuint64_t strides[3] = {128, 256, sig_stride};
+    const cuuint32_t box[4] = {32, 1, 128, 1}, es[4] = {1, 1, 1, 1};
+    r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    const cuuint64_t dims[3] = {32, rows, static_cast<cuuint64_t>(pl->batch)};
+    const cuuint64_t strides[2] = {128, sig_stride};
+    const cuuint32_t box[3] = {32, 128, 1}, es[3] = {1, 1, 1};
+    r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  return r == CUDA_SUCCESS;
+}
+
 long long* g_tc_trace = nullptr;  // diagnostics: sftgpu_debug_set_tc_trace
 
 void run_tc(sftgpu_plan* pl, const void* x, long long ld_x, void* out, long long ld_out, cudaStream_t st) {
-  tck::TcParams P = pl->tcp;
+  tck::TcParams& C = pl->tcp;
+  if (pl->tc_map_out != out || pl->tc_map_ld != ld_out) {
+    C.use_tma = make_out_map(pl, out, ld_out, &C.out_map) ? 1 : 0;
+    pl->tc_map_out = out;
+    pl->tc_map_ld = ld_out;
+  }
+  tck::TcParams P = C;
   P.x = static_cast<const float*>(x);
   P.out = static_cast<float*>(out);
   P.ld_x = ld_x;
   P.ld_out = ld_out;
   const size_t rowb = static_cast<size_t>(ld_out) * sizeof(float) * (P.cplx ? 2 : 1);
   P.vec_ok = (reinterpret_cast<uintptr_t>(out) % 16 == 0 && rowb % 16 == 0) ? 1 : 0;
+  if (const char* e = std::getenv("SFTGPU_TC_NO_TMA")) P.use_tma = e[0] == '1' ? 0 : P.use_tma;
   P.trace = g_tc_trace;
   cuda_check(tck::launch_tc(P, pl->tc_grid, st), "sft_tc_kernel launch");
 }

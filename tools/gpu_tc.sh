@@ -1,2 +1,3 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
-for w in morlet_multiply_batch scalogram; do timeout 600 python bench.py --workload $w > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; tail -c 600 gpurun_out/bench_$w.json; echo; done
+timeout 120 python -m pytest tests/test_gpu_tc.py -x -q 2>&1 | tail -2
+timeout 120 python tools/tc_trace.py 2>&1 | sed -n '1,1p;18,22p'
+timeout 300 python tools/tc_probe.py 2>&1 | tail -3
