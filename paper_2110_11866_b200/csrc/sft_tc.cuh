@@ -29,11 +29,11 @@
 //               half of the orders, warps 4-7 the rest) -> states into TMEM, then warp 0
 //               issues the chunk-state GEMM; warm-up tiles only reduce their aggregates
 //               into the fp64 tile carry
-//   warps 8-11  epilogue: TMEM -> swizzled staging (accumulator released) -> coalesced
-//               16-byte stores
+//   warps 8-11  epilogue: TMEM -> swizzled staging (accumulator released) -> TMA store;
+//               warp 8 issues the merged GEMM of the next tile first
 //   warps 12-15 loader: coalesced cp.async into a ring of padded staging rows; each
 //               thread then reads its chunk row, splits it (TF32 head / remainder) and
-//               tcgen05.st's it; warp 12 then issues the merged GEMM of the tile
+//               tcgen05.st's it
 // Pipelines (mbarriers): TMEM X operands, chunk states and accumulators double-buffered;
 // loader staging ring; tile carry double-buffered.
 #pragma once
@@ -48,7 +48,7 @@
 namespace tck {
 
 struct Misc {
-  uint64_t xfree[2], g1done[2], dfree[2], g2done[2];
+  uint64_t xfull[2], xfree[2], g1done[2], dfree[2], g2done[2];
   uint32_t tmem;
   double2 cy[2][kMaxOrd];      // tile carry (state entering the tile), fp64, by tile parity
   float2 wtot[2][4][kMaxOrd];  // per-warp chunk-aggregate totals (by tile parity)
@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
   }
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&M.xfull[b], 128);
       umma::mbar_init(&M.xfree[b], 1);
       umma::mbar_init(&M.g1done[b], 1);
       umma::mbar_init(&M.dfree[b], 128);
@@ -239,7 +240,6 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     unsigned long long keep, first;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(first));
-    const uint32_t idm = umma::idesc_tf32(128, NO + 16), ida = umma::idesc_tf32(128, 16);
     auto issue = [&](const Walk& w, int buf) {
       if (w.valid) {
         const float* xs = P.x + w.sig * P.ld_x;
@@ -286,35 +286,8 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       if (!warm) row_to_tmem(sb + 32 * kStgRow, lane, tx + 64);
       umma::tmem_wait_st();
       umma::fence_before();
-      bar_named(4, 128);  // all four lane quarters of the tile are in TMEM
+      umma::mbar_arrive(&M.xfull[b]);
       if (lane == 0) trace_ev(P, gt, 1);
-      if (q == 0) {
-        // merged GEMM (outputs + aggregates; warm tiles: aggregates of the lead stream)
-        // into accumulator b once the epilogue / scan have released it
-        if (gt >= 2) umma::mbar_wait(&M.dfree[b], static_cast<uint32_t>(((gt >> 1) - 1) & 1));
-        __syncwarp();
-        umma::fence_after();
-        const uint32_t d = tmem + (b ? kTD1 : kTD0), x = tmem + kTX + 128 * b;
-        if (!warm) {
-          merged_k<0>(dbase, d, x, idm);
-          merged_k<1>(dbase, d, x, idm);
-          merged_k<2>(dbase, d, x, idm);
-          merged_k<3>(dbase, d, x, idm);
-        } else if (NO == 64) {
-          warm_k<0, 64>(dbase, d + 64, x, ida);
-          warm_k<1, 64>(dbase, d + 64, x, ida);
-          warm_k<2, 64>(dbase, d + 64, x, ida);
-          warm_k<3, 64>(dbase, d + 64, x, ida);
-        } else {
-          warm_k<0, 32>(dbase, d + 32, x, ida);
-          warm_k<1, 32>(dbase, d + 32, x, ida);
-          warm_k<2, 32>(dbase, d + 32, x, ida);
-          warm_k<3, 32>(dbase, d + 32, x, ida);
-        }
-        umma::commit_elect(&M.g1done[b]);
-        umma::commit_elect(&M.xfree[b]);
-        if (lane == 0) trace_ev(P, gt, 2);
-      }
       __syncwarp();  // every lane has read its row before the ring slot is refilled
       w.advance(P);
     }
@@ -326,10 +299,50 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     unsigned char* const stgo = sm + kStage;
     const int halves = P.cplx ? 2 : 1;
     const int cw = P.cplx ? 2 : 1;
-    Walk w;
+    const uint32_t idm = umma::idesc_tf32(128, NO + 16), ida = umma::idesc_tf32(128, 16);
+    // warp 8 also issues the merged GEMM (outputs + aggregates; warm tiles: aggregates of
+    // the lead stream) of tile g into accumulator g & 1 once its operands are in TMEM and
+    // the accumulator is free, one tile ahead of the epilogue it then runs
+    auto merged = [&](const Walk& wm, long long g) {
+      const int b = static_cast<int>(g & 1);
+      umma::mbar_wait(&M.xfull[b], static_cast<uint32_t>((g >> 1) & 1));
+      if (g >= 2) umma::mbar_wait(&M.dfree[b], static_cast<uint32_t>(((g >> 1) - 1) & 1));
+      __syncwarp();
+      umma::fence_after();
+      const uint32_t d = tmem + (b ? kTD1 : kTD0), x = tmem + kTX + 128 * b;
+      if (!wm.warm(P)) {
+        merged_k<0>(dbase, d, x, idm);
+        merged_k<1>(dbase, d, x, idm);
+        merged_k<2>(dbase, d, x, idm);
+        merged_k<3>(dbase, d, x, idm);
+      } else if (NO == 64) {
+        warm_k<0, 64>(dbase, d + 64, x, ida);
+        warm_k<1, 64>(dbase, d + 64, x, ida);
+        warm_k<2, 64>(dbase, d + 64, x, ida);
+        warm_k<3, 64>(dbase, d + 64, x, ida);
+      } else {
+        warm_k<0, 32>(dbase, d + 32, x, ida);
+        warm_k<1, 32>(dbase, d + 32, x, ida);
+        warm_k<2, 32>(dbase, d + 32, x, ida);
+        warm_k<3, 32>(dbase, d + 32, x, ida);
+      }
+      umma::commit_elect(&M.g1done[b]);
+      umma::commit_elect(&M.xfree[b]);
+      if (lane == 0) trace_ev(P, g, 2);
+    };
+    Walk w, wn;
     w.begin(P);
+    wn.begin(P);
+    if (ew == 0 && wn.valid) {
+      merged(wn, 0);
+      wn.advance(P);
+    }
     long long u = 0;
     for (long long gt = 0; w.valid; w.advance(P), ++gt) {
+      if (ew == 0 && wn.valid) {
+        merged(wn, gt + 1);
+        wn.advance(P);
+      }
       if (w.warm(P)) continue;
       const int s = static_cast<int>(u & 1);
       umma::mbar_wait(&M.g2done[s], static_cast<uint32_t>((u >> 1) & 1));
