@@ -48,7 +48,7 @@
 namespace tck {
 
 struct Misc {
-  uint64_t xfull[2], xfree[2], g1done[2], dfree[2], g2done[2];
+  uint64_t xfull, xfree, g1done[kNDBuf], dfree[kNDBuf], g2done[2];
   uint32_t tmem;
   double2 cy[2][kMaxOrd];      // tile carry (state entering the tile), fp64, by tile parity
   float2 wtot[2][4][kMaxOrd];  // per-warp chunk-aggregate totals (by tile parity)
@@ -213,13 +213,13 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     for (int i = tid; i < static_cast<int>(kImage / 16); i += kThreads) dst[i] = __ldg(P.image + i);
   }
   if (tid == 0) {
-    for (int b = 0; b < 2; ++b) {
-      umma::mbar_init(&M.xfull[b], 128);
-      umma::mbar_init(&M.xfree[b], 1);
+    umma::mbar_init(&M.xfull, 128);
+    umma::mbar_init(&M.xfree, 1);
+    for (int b = 0; b < kNDBuf; ++b) {
       umma::mbar_init(&M.g1done[b], 1);
       umma::mbar_init(&M.dfree[b], 128);
-      umma::mbar_init(&M.g2done[b], 1);
     }
+    for (int b = 0; b < 2; ++b) umma::mbar_init(&M.g2done[b], 1);
     umma::mbar_fence_init();
   }
   if (tid < kMaxOrd) M.cy[0][tid] = make_double2(0.0, 0.0);
@@ -274,19 +274,19 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       if (wi.valid) wi.advance(P);
       asm volatile("cp.async.wait_group %0;" ::"n"(kLoadAhead) : "memory");
       __syncwarp();
-      const int b = static_cast<int>(gt & 1);
-      if (gt >= 2) umma::mbar_wait(&M.xfree[b], static_cast<uint32_t>(((gt >> 1) - 1) & 1));
+      // the single X stage is free once the merged GEMM of the previous tile has read it
+      if (gt >= 1) umma::mbar_wait(&M.xfree, static_cast<uint32_t>((gt - 1) & 1));
       __syncwarp();
       umma::fence_after();
       if (lane == 0) trace_ev(P, gt, 0);
       const float* sb = stg + static_cast<int>(gt % (kLoadAhead + 1)) * 2 * 32 * kStgRow;
-      const uint32_t tx = tmem + lrow + kTX + 128 * b;
+      const uint32_t tx = tmem + lrow + kTX;
       const bool warm = w.warm(P);
       row_to_tmem(sb, lane, tx);
       if (!warm) row_to_tmem(sb + 32 * kStgRow, lane, tx + 64);
       umma::tmem_wait_st();
       umma::fence_before();
-      umma::mbar_arrive(&M.xfull[b]);
+      umma::mbar_arrive(&M.xfull);
       if (lane == 0) trace_ev(P, gt, 1);
       __syncwarp();  // every lane has read its row before the ring slot is refilled
       w.advance(P);
@@ -301,15 +301,15 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     const int cw = P.cplx ? 2 : 1;
     const uint32_t idm = umma::idesc_tf32(128, NO + 16), ida = umma::idesc_tf32(128, 16);
     // warp 8 also issues the merged GEMM (outputs + aggregates; warm tiles: aggregates of
-    // the lead stream) of tile g into accumulator g & 1 once its operands are in TMEM and
+    // the lead stream) of tile g into accumulator g % 3 once its operands are in TMEM and
     // the accumulator is free, one tile ahead of the epilogue it then runs
     auto merged = [&](const Walk& wm, long long g) {
-      const int b = static_cast<int>(g & 1);
-      umma::mbar_wait(&M.xfull[b], static_cast<uint32_t>((g >> 1) & 1));
-      if (g >= 2) umma::mbar_wait(&M.dfree[b], static_cast<uint32_t>(((g >> 1) - 1) & 1));
+      const int b = static_cast<int>(g % kNDBuf);
+      umma::mbar_wait(&M.xfull, static_cast<uint32_t>(g & 1));
+      if (g >= kNDBuf) umma::mbar_wait(&M.dfree[b], static_cast<uint32_t>((g / kNDBuf - 1) & 1));
       __syncwarp();
       umma::fence_after();
-      const uint32_t d = tmem + (b ? kTD1 : kTD0), x = tmem + kTX + 128 * b;
+      const uint32_t d = tmem + kTD + kTDStride * b, x = tmem + kTX;
       if (!wm.warm(P)) {
         merged_k<0>(dbase, d, x, idm);
         merged_k<1>(dbase, d, x, idm);
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
         warm_k<3, 32>(dbase, d + 32, x, ida);
       }
       umma::commit_elect(&M.g1done[b]);
-      umma::commit_elect(&M.xfree[b]);
+      umma::commit_elect(&M.xfree);
       if (lane == 0) trace_ev(P, g, 2);
     };
     Walk w, wn;
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       if (c == 0) trace_ev(P, gt, 6);
       __syncwarp();
       umma::fence_after();
-      const uint32_t dcol = (gt & 1) ? kTD1 : kTD0;
+      const uint32_t dcol = kTD + kTDStride * static_cast<uint32_t>(gt % kNDBuf);
       // the previous tile's TMA stores must have read the staging area
       if (c == 0 && P.use_tma) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       bar_named(3, 128);
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
               make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       }
       umma::fence_before();
-      umma::mbar_arrive(&M.dfree[gt & 1]);
+      umma::mbar_arrive(&M.dfree[gt % kNDBuf]);
       if (c == 0) trace_ev(P, gt, 14);
       ++u;
       const long long o0 = w.o0(P), cnt = w.cnt;
@@ -425,14 +425,15 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     w.begin(P);
     long long u = 0;
     for (long long gt = 0; w.valid; ++gt) {
-      const int b = static_cast<int>(gt & 1);
-      umma::mbar_wait(&M.g1done[b], static_cast<uint32_t>((gt >> 1) & 1));
+      const int b = static_cast<int>(gt & 1);  // carry / warp-total double buffers
+      const int db = static_cast<int>(gt % kNDBuf);
+      umma::mbar_wait(&M.g1done[db], static_cast<uint32_t>((gt / kNDBuf) & 1));
       if (tid == 0) trace_ev(P, gt, 3);
       __syncwarp();
       umma::fence_after();
       const bool warm = w.warm(P);
       uint32_t a8[8];
-      umma::tmem_ld8(tmem + lrow + (b ? kTD1 : kTD0) + NO + 2 * p0, a8);  // this set's orders
+      umma::tmem_ld8(tmem + lrow + kTD + kTDStride * db + NO + 2 * p0, a8);  // this set's orders
       umma::tmem_wait_ld();
       if (tid == 0) trace_ev(P, gt, 8);
       if (warm) {
@@ -441,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
         bar_named(5, 256);
         if (warp == 0) {
           __syncwarp();
-          if (lane == 0) umma::mbar_arrive_cnt(&M.dfree[b], 128);
+          if (lane == 0) umma::mbar_arrive_cnt(&M.dfree[db], 128);
         }
       }
       float2 inc[4];
@@ -534,7 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
         if (warp == 0) {
           // chunk-state GEMM: D[:, 0:NO) += S . C^T (3xTF32)
           umma::fence_after();
-          const uint32_t d = tmem + (b ? kTD1 : kTD0), a = tmem + kTSS + 32 * s;
+          const uint32_t d = tmem + kTD + kTDStride * db, a = tmem + kTSS + 32 * s;
           const uint32_t ids = umma::idesc_tf32(128, NO);
           umma::mma_tf32_ts<kBC>(d, a, dbase, ids, 1);  // S_h . C_h
           umma::mma_tf32_ts<kBC + 32>(d, a + 8, dbase, ids, 1);
