@@ -29,11 +29,11 @@
 //               half of the orders, warps 4-7 the rest) -> states into TMEM, then warp 0
 //               issues the chunk-state GEMM; warm-up tiles only reduce their aggregates
 //               into the fp64 tile carry
-//   warps 8-11  epilogue: TMEM -> swizzled staging (accumulator released) -> TMA store;
-//               warp 8 issues the merged GEMM of the next tile first
+//   warps 8-11  epilogue: TMEM -> swizzled staging (accumulator released) -> coalesced
+//               16-byte stores
 //   warps 12-15 loader: coalesced cp.async into a ring of padded staging rows; each
 //               thread then reads its chunk row, splits it (TF32 head / remainder) and
-//               tcgen05.st's it
+//               tcgen05.st's it; warp 12 then issues the merged GEMM of the tile
 // Pipelines (mbarriers): TMEM X operands, chunk states and accumulators double-buffered;
 // loader staging ring; tile carry double-buffered.
 #pragma once
@@ -48,7 +48,7 @@
 namespace tck {
 
 struct Misc {
-  uint64_t xfull, xfree, g1done[kNDBuf], dfree[kNDBuf], g2done[2];
+  uint64_t xfree[2], g1done[2], dfree[2], g2done[2];
   uint32_t tmem;
   double2 cy[2][kMaxOrd];      // tile carry (state entering the tile), fp64, by tile parity
   float2 wtot[2][4][kMaxOrd];  // per-warp chunk-aggregate totals (by tile parity)
@@ -213,13 +213,12 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     for (int i = tid; i < static_cast<int>(kImage / 16); i += kThreads) dst[i] = __ldg(P.image + i);
   }
   if (tid == 0) {
-    umma::mbar_init(&M.xfull, 128);
-    umma::mbar_init(&M.xfree, 1);
-    for (int b = 0; b < kNDBuf; ++b) {
+    for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&M.xfree[b], 1);
       umma::mbar_init(&M.g1done[b], 1);
       umma::mbar_init(&M.dfree[b], 128);
+      umma::mbar_init(&M.g2done[b], 1);
     }
-    for (int b = 0; b < 2; ++b) umma::mbar_init(&M.g2done[b], 1);
     umma::mbar_fence_init();
   }
   if (tid < kMaxOrd) M.cy[0][tid] = make_double2(0.0, 0.0);
@@ -240,6 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     unsigned long long keep, first;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(first));
+    const uint32_t idm = umma::idesc_tf32(128, NO + 16), ida = umma::idesc_tf32(128, 16);
     auto issue = [&](const Walk& w, int buf) {
       if (w.valid) {
         const float* xs = P.x + w.sig * P.ld_x;
@@ -274,20 +274,47 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       if (wi.valid) wi.advance(P);
       asm volatile("cp.async.wait_group %0;" ::"n"(kLoadAhead) : "memory");
       __syncwarp();
-      // the single X stage is free once the merged GEMM of the previous tile has read it
-      if (gt >= 1) umma::mbar_wait(&M.xfree, static_cast<uint32_t>((gt - 1) & 1));
+      const int b = static_cast<int>(gt & 1);
+      if (gt >= 2) umma::mbar_wait(&M.xfree[b], static_cast<uint32_t>(((gt >> 1) - 1) & 1));
       __syncwarp();
       umma::fence_after();
       if (lane == 0) trace_ev(P, gt, 0);
       const float* sb = stg + static_cast<int>(gt % (kLoadAhead + 1)) * 2 * 32 * kStgRow;
-      const uint32_t tx = tmem + lrow + kTX;
+      const uint32_t tx = tmem + lrow + kTX + 128 * b;
       const bool warm = w.warm(P);
       row_to_tmem(sb, lane, tx);
       if (!warm) row_to_tmem(sb + 32 * kStgRow, lane, tx + 64);
       umma::tmem_wait_st();
       umma::fence_before();
-      umma::mbar_arrive(&M.xfull);
+      bar_named(4, 128);  // all four lane quarters of the tile are in TMEM
       if (lane == 0) trace_ev(P, gt, 1);
+      if (q == 0) {
+        // merged GEMM (outputs + aggregates; warm tiles: aggregates of the lead stream)
+        // into accumulator b once the epilogue / scan have released it
+        if (gt >= 2) umma::mbar_wait(&M.dfree[b], static_cast<uint32_t>(((gt >> 1) - 1) & 1));
+        __syncwarp();
+        umma::fence_after();
+        const uint32_t d = tmem + (b ? kTD1 : kTD0), x = tmem + kTX + 128 * b;
+        if (!warm) {
+          merged_k<0>(dbase, d, x, idm);
+          merged_k<1>(dbase, d, x, idm);
+          merged_k<2>(dbase, d, x, idm);
+          merged_k<3>(dbase, d, x, idm);
+        } else if (NO == 64) {
+          warm_k<0, 64>(dbase, d + 64, x, ida);
+          warm_k<1, 64>(dbase, d + 64, x, ida);
+          warm_k<2, 64>(dbase, d + 64, x, ida);
+          warm_k<3, 64>(dbase, d + 64, x, ida);
+        } else {
+          warm_k<0, 32>(dbase, d + 32, x, ida);
+          warm_k<1, 32>(dbase, d + 32, x, ida);
+          warm_k<2, 32>(dbase, d + 32, x, ida);
+          warm_k<3, 32>(dbase, d + 32, x, ida);
+        }
+        umma::commit_elect(&M.g1done[b]);
+        umma::commit_elect(&M.xfree[b]);
+        if (lane == 0) trace_ev(P, gt, 2);
+      }
       __syncwarp();  // every lane has read its row before the ring slot is refilled
       w.advance(P);
     }
@@ -299,57 +326,17 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     unsigned char* const stgo = sm + kStage;
     const int halves = P.cplx ? 2 : 1;
     const int cw = P.cplx ? 2 : 1;
-    const uint32_t idm = umma::idesc_tf32(128, NO + 16), ida = umma::idesc_tf32(128, 16);
-    // warp 8 also issues the merged GEMM (outputs + aggregates; warm tiles: aggregates of
-    // the lead stream) of tile g into accumulator g % 3 once its operands are in TMEM and
-    // the accumulator is free, one tile ahead of the epilogue it then runs
-    auto merged = [&](const Walk& wm, long long g) {
-      const int b = static_cast<int>(g % kNDBuf);
-      umma::mbar_wait(&M.xfull, static_cast<uint32_t>(g & 1));
-      if (g >= kNDBuf) umma::mbar_wait(&M.dfree[b], static_cast<uint32_t>((g / kNDBuf - 1) & 1));
-      __syncwarp();
-      umma::fence_after();
-      const uint32_t d = tmem + kTD + kTDStride * b, x = tmem + kTX;
-      if (!wm.warm(P)) {
-        merged_k<0>(dbase, d, x, idm);
-        merged_k<1>(dbase, d, x, idm);
-        merged_k<2>(dbase, d, x, idm);
-        merged_k<3>(dbase, d, x, idm);
-      } else if (NO == 64) {
-        warm_k<0, 64>(dbase, d + 64, x, ida);
-        warm_k<1, 64>(dbase, d + 64, x, ida);
-        warm_k<2, 64>(dbase, d + 64, x, ida);
-        warm_k<3, 64>(dbase, d + 64, x, ida);
-      } else {
-        warm_k<0, 32>(dbase, d + 32, x, ida);
-        warm_k<1, 32>(dbase, d + 32, x, ida);
-        warm_k<2, 32>(dbase, d + 32, x, ida);
-        warm_k<3, 32>(dbase, d + 32, x, ida);
-      }
-      umma::commit_elect(&M.g1done[b]);
-      umma::commit_elect(&M.xfree);
-      if (lane == 0) trace_ev(P, g, 2);
-    };
-    Walk w, wn;
+    Walk w;
     w.begin(P);
-    wn.begin(P);
-    if (ew == 0 && wn.valid) {
-      merged(wn, 0);
-      wn.advance(P);
-    }
     long long u = 0;
     for (long long gt = 0; w.valid; w.advance(P), ++gt) {
-      if (ew == 0 && wn.valid) {
-        merged(wn, gt + 1);
-        wn.advance(P);
-      }
       if (w.warm(P)) continue;
       const int s = static_cast<int>(u & 1);
       umma::mbar_wait(&M.g2done[s], static_cast<uint32_t>((u >> 1) & 1));
       if (c == 0) trace_ev(P, gt, 6);
       __syncwarp();
       umma::fence_after();
-      const uint32_t dcol = kTD + kTDStride * static_cast<uint32_t>(gt % kNDBuf);
+      const uint32_t dcol = (gt & 1) ? kTD1 : kTD0;
       // the previous tile's TMA stores must have read the staging area
       if (c == 0 && P.use_tma) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       bar_named(3, 128);
@@ -365,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
               make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       }
       umma::fence_before();
-      umma::mbar_arrive(&M.dfree[gt % kNDBuf]);
+      umma::mbar_arrive(&M.dfree[gt & 1]);
       if (c == 0) trace_ev(P, gt, 14);
       ++u;
       const long long o0 = w.o0(P), cnt = w.cnt;
@@ -425,15 +412,14 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     w.begin(P);
     long long u = 0;
     for (long long gt = 0; w.valid; ++gt) {
-      const int b = static_cast<int>(gt & 1);  // carry / warp-total double buffers
-      const int db = static_cast<int>(gt % kNDBuf);
-      umma::mbar_wait(&M.g1done[db], static_cast<uint32_t>((gt / kNDBuf) & 1));
+      const int b = static_cast<int>(gt & 1);
+      umma::mbar_wait(&M.g1done[b], static_cast<uint32_t>((gt >> 1) & 1));
       if (tid == 0) trace_ev(P, gt, 3);
       __syncwarp();
       umma::fence_after();
       const bool warm = w.warm(P);
       uint32_t a8[8];
-      umma::tmem_ld8(tmem + lrow + kTD + kTDStride * db + NO + 2 * p0, a8);  // this set's orders
+      umma::tmem_ld8(tmem + lrow + (b ? kTD1 : kTD0) + NO + 2 * p0, a8);  // this set's orders
       umma::tmem_wait_ld();
       if (tid == 0) trace_ev(P, gt, 8);
       if (warm) {
@@ -442,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
         bar_named(5, 256);
         if (warp == 0) {
           __syncwarp();
-          if (lane == 0) umma::mbar_arrive_cnt(&M.dfree[db], 128);
+          if (lane == 0) umma::mbar_arrive_cnt(&M.dfree[b], 128);
         }
       }
       float2 inc[4];
@@ -535,7 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
         if (warp == 0) {
           // chunk-state GEMM: D[:, 0:NO) += S . C^T (3xTF32)
           umma::fence_after();
-          const uint32_t d = tmem + kTD + kTDStride * db, a = tmem + kTSS + 32 * s;
+          const uint32_t d = tmem + (b ? kTD1 : kTD0), a = tmem + kTSS + 32 * s;
           const uint32_t ids = umma::idesc_tf32(128, NO);
           umma::mma_tf32_ts<kBC>(d, a, dbase, ids, 1);  // S_h . C_h
           umma::mma_tf32_ts<kBC + 32>(d, a + 8, dbase, ids, 1);

@@ -29,12 +29,9 @@ constexpr uint32_t kLStage = kImage;                     // loader staging, 4 wa
 constexpr uint32_t kStage = kLStage + 4 * kStgWarp;      // epilogue staging (128 rows x 128 B)
 constexpr uint32_t kMisc = kStage + 32768;  // epilogue staging: two halves
 constexpr uint32_t kSmemBytes = kMisc + 1024 + 1024;  // misc + alignment slack
-// TMEM columns (512 allocated): X operands [xl_h, xl_l, xt_h, xt_l] x 32 (one stage:
-// refilled as soon as the merged GEMM has read it), chunk states [2][S_h (16) | S_l (16)],
-// accumulators [3][outputs | aggregates] (3 deep: the scan, chunk-state GEMM and epilogue
-// of neighbouring tiles overlap)
-constexpr uint32_t kTX = 0, kTSS = 128, kTD = 192, kTDStride = 96;
-constexpr int kNDBuf = 3;
+// TMEM columns (512 allocated): X operands [stage][xl_h, xl_l, xt_h, xt_l] x 32,
+// chunk states [2][S_h (16) | S_l (16)], accumulators [2][outputs | aggregates]
+constexpr uint32_t kTX = 0, kTSS = 256, kTD0 = 320, kTD1 = 416;
 
 struct TcParams {
   CUtensorMap out_map;  // TMA view of the output (see run_tc); valid when use_tma
