@@ -1,11 +1,11 @@
-// K4 / K5 — the paper's data-parallel sliding sum h[n] = sum_{k<L} f[n+k] on the GPU
+// K5 / K6 — the paper's data-parallel sliding sum h[n] = sum_{k<L} f[n+k] on the GPU
 // (§IV, Algorithms 1-3). The reference only simulates these on CPU threads
 // (proj/include/sft/sliding_sum.hpp:89-234); here they run as real kernels with the
 // exact same addition trees, so results are bit-identical to the reference's for
 // integers and doubles.
-//   K4 flat doubling (Alg. 1): R = ceil(log2(L+1)) bulk rounds over double buffers,
+//   K5 flat doubling (Alg. 1): R = ceil(log2(L+1)) bulk rounds over double buffers,
 //      g'[i] = g[i] + g[i+2^r], h'[i] = bit(L,r) ? g[i] + h[i+2^r] : h[i] (0 past the end).
-//   K5 blocked8 (Alg. 2-3): (16,8) shared-memory tiles, three doubling rounds per base-8
+//   K6 blocked8 (Alg. 2-3): (16,8) shared-memory tiles, three doubling rounds per base-8
 //      digit of L, transposed write-back so stride-8 neighbours become adjacent, final
 //      un-permute through the blocked layout.
 #pragma once

@@ -1,5 +1,2 @@
 timeout 120 python -m pytest tests/test_gpu_tc.py -x -q 2>&1 | tail -1
-for i in 1 2; do
 timeout 300 python tools/tc_probe.py 1 2>&1 | tail -1
-SFTGPU_TC_NO_TMA=1 timeout 300 python tools/tc_probe.py 1 2>&1 | tail -1
-done
