@@ -66,7 +66,7 @@ struct Walk {
     obase = ch * P.chunk_len;
     cnt = P.count - obase < P.chunk_len ? P.count - obase : P.chunk_len;
     ntiles = P.warm_tiles + (cnt + kTile - 1) / kTile;
-    t = 0;
+    t = ch == 0 ? P.skip0 : 0;  // skipped constant warm-up tiles (carry in closed form)
   }
   __device__ void begin(const TcParams& P) {
     item = blockIdx.x;
@@ -81,6 +81,16 @@ struct Walk {
   __device__ long long o0(const TcParams& P) const { return (t - P.warm_tiles) * kTile; }
   __device__ bool last(const TcParams& P) const { return t + 1 == ntiles; }
 };
+
+// fp64 state entering the first processed tile of `item` for order p: the closed-form
+// contribution of the skipped constant warm-up tiles (0 when none are skipped)
+__device__ __forceinline__ double2 item_carry(const TcParams& P, long long item, int p) {
+  if (item >= P.n_items || P.skip0 == 0 || P.boundary == 0) return make_double2(0.0, 0.0);
+  const long long sig = item / P.n_chunks;
+  if (item - sig * P.n_chunks != 0) return make_double2(0.0, 0.0);
+  const double v = static_cast<double>(__ldg(P.x + sig * P.ld_x));
+  return make_double2(v * P.g0[p].x, v * P.g0[p].y);
+}
 
 __device__ __forceinline__ void trace_ev(const TcParams& P, long long gt, int ev) {
   if (P.trace && blockIdx.x == 0 && gt < 64) P.trace[gt * 16 + ev] = clock64();
@@ -221,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     }
     umma::mbar_fence_init();
   }
-  if (tid < kMaxOrd) M.cy[0][tid] = make_double2(0.0, 0.0);
+  if (tid < kMaxOrd) M.cy[0][tid] = item_carry(P, blockIdx.x, tid);
   if (warp == 0) umma::tmem_alloc(&M.tmem, 512);
   umma::fence_proxy_async();
   umma::fence_before();
@@ -545,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
                            fma(z.x, T.y, fma(z.y, T.x, static_cast<double>(t.y))));
         }
         const double2 cy = cyin[p];
-        M.cy[b ^ 1][p] = w.last(P) ? make_double2(0.0, 0.0)
+        M.cy[b ^ 1][p] = w.last(P) ? item_carry(P, w.item + gridDim.x, p)
                                    : make_double2(fma(zt.x, cy.x, fma(-zt.y, cy.y, T.x)),
                                                   fma(zt.x, cy.y, fma(zt.y, cy.x, T.y)));
       }

@@ -46,6 +46,11 @@ struct TcParams {
   float2 zs[kMaxOrd][6];  // z^{32 * 2^k} (k < 5), z^{1024}
   double2 z1024[kMaxOrd];
   double2 zT[kMaxOrd];  // z^{4096}
+  // Leading warm-up tiles of a signal's first chunk whose lead samples all lie in the
+  // uniform boundary region (before sample 0) are not processed: the state they build is
+  // v * g0[p], v = x[0] (clamp) or 0 (zero boundary), g0 = sum_{e < E} z^e (host, fp64).
+  int skip0;
+  double2 g0[kMaxOrd];
 };
 
 cudaError_t launch_tc(const TcParams& p, int grid, cudaStream_t s);

@@ -587,6 +587,23 @@ bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
   P.n_chunks = (pl->count + P.chunk_len - 1) / P.chunk_len;
   P.n_items = pl->batch * P.n_chunks;
   P.warm_tiles = (2LL * K + tck::kTile - 1) / tck::kTile;
+  {
+    // leading warm-up tiles of chunk 0 whose lead samples j = lo + o + K are all < 0: the
+    // zeros before the warm start (Z positions) then the boundary value v; state after
+    // them = v * sum_{e < E} z^e with E = 4096 skip - Z
+    const long long W = P.warm_tiles, jfirst = pl->lo + K - W * tck::kTile;
+    const long long skip = jfirst < 0 ? std::min(W, (-jfirst) / tck::kTile) : 0;
+    const long long Z = W * tck::kTile - 2LL * K, E = skip * tck::kTile - Z;
+    P.skip0 = static_cast<int>(skip);
+    for (int p = 0; p < nord; ++p) {
+      cd g(0.0, 0.0);
+      if (E > 0) {
+        const cd z = zpow(alpha, ords[p].omega, 1.0), zE = zpow(alpha, ords[p].omega, static_cast<double>(E));
+        g = std::abs(1.0 - z) < 1e-12 ? cd(static_cast<double>(E), 0.0) : (1.0 - zE) / (1.0 - z);
+      }
+      P.g0[p] = make_double2(g.real(), g.imag());
+    }
+  }
   P.n = pl->n;
   P.lo = pl->lo;
   P.count = pl->count;

@@ -64,6 +64,24 @@ def test_tc_boundaries_and_offset(sft, O, boundary):
         assert rel_max(tc[b], oracle_transform(O, xh[b], boundary, spec)) < 1e-5
 
 
+@pytest.mark.parametrize("boundary", [0, 1])
+def test_tc_skipped_constant_warmup(sft, O, boundary):
+    """Config-4 geometry (sigma = 8192, n0 = 5): six leading warm-up tiles of every signal
+    read only boundary samples and are replaced by their closed-form state; both boundary
+    policies, and a DC offset so the clamped boundary value is far from zero (x + 1: larger
+    offsets are ill-conditioned in fp32 for every kernel, K1 included, tools/dc_probe.py)."""
+    import torch
+
+    spec = sft.make_transform_spec("MMS5P3", 8192.0, 10.0, sft.TransformOptions(precision=0))
+    n = 102400
+    x = O.make_test_signal(O.SEEDED_NOISE, n, 11) + 1.0
+    xb = torch.tensor(np.stack([x, 0.5 * x]), dtype=torch.float32, device="cuda")
+    _, tc = _run(sft, spec, xb, "tc", boundary)
+    xh = xb.double().cpu().numpy()
+    for b in range(2):
+        assert rel_max(tc[b], oracle_transform(O, xh[b], boundary, spec)) < 1e-5
+
+
 def test_tc_ranged_plan_matches_full(sft, O):
     """Output-range plans (chunk sharding with halo) reproduce the full transform."""
     spec = sft.make_transform_spec("MDS5P6", 2000.0, 10.0, sft.TransformOptions(precision=0))
