@@ -242,9 +242,10 @@ int sftgpu_transform_execute_host(sftgpu_plan* plan, const void* x_host, void* o
                                   void* stream);
 /* Pipelined variant for streams of host buffers: enqueues H2D of x_host, the transform
  * and D2H into out_host on the plan's internal copy-in / compute / copy-out streams
- * (three staging slots) and returns without waiting, so the copies of neighbouring calls
- * overlap this call's kernel. Work queued on `stream` before the call runs first, and
- * `stream` waits for this call's D2H: after cudaStreamSynchronize(stream) (or
+ * (three staging slots) and returns without waiting, so the copy-in of the next call,
+ * this call's kernel and the previous call's copy-out overlap. x_host must hold its data
+ * when the call is made (it is not ordered after work queued on `stream`); `stream`
+ * waits for this call's D2H: after cudaStreamSynchronize(stream) (or
  * sftgpu_plan_synchronize) out_host holds the result. x_host must stay valid and
  * out_host untouched until then; host buffers must be pinned for the copies to overlap.
  * Do not interleave with sftgpu_transform_execute on the same plan while calls are in

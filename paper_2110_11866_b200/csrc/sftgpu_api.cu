@@ -1353,9 +1353,9 @@ int sftgpu_transform_execute_host_async(sftgpu_plan* pl, const void* x_host, voi
     size_t cap = sl.d_x ? xb : 0, capo = sl.d_out ? ob : 0;
     ensure_buffer(&sl.d_x, &cap, xb, "cudaMalloc async staging x");
     ensure_buffer(&sl.d_out, &capo, ob, "cudaMalloc async staging out");
-    // work already queued on the caller's stream comes first
-    cuda_check(cudaEventRecord(pl->ev_entry, user), "event record");
-    cuda_check(cudaStreamWaitEvent(pl->s_in, pl->ev_entry, 0), "stream wait");
+    // no entry dependency on the caller's stream: that stream waits for every earlier
+    // call's copy-out, and ordering copy-in behind it would serialise the pipeline
+    // (x_host is host data, ready at call time)
     // copy-in may overwrite this slot's input once the slot's previous kernel has read it
     cuda_check(cudaStreamWaitEvent(pl->s_in, sl.ev_comp, 0), "stream wait");
     cuda_check(cudaMemcpyAsync(sl.d_x, x_host, xb, cudaMemcpyHostToDevice, pl->s_in), "H2D");

@@ -93,12 +93,20 @@ class Signal:
         return self.size()
 
 
-def _torch():
-    import torch
+_TORCH = None
 
-    if not torch.cuda.is_available():
-        raise SftGpuError("no CUDA device available (libsftgpu has no CPU fallback)")
-    return torch
+
+def _torch():
+    """torch, once a CUDA device is known to exist (checked once: torch.cuda.is_available()
+    queries the driver and costs microseconds on the streaming path)."""
+    global _TORCH
+    if _TORCH is None:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise SftGpuError("no CUDA device available (libsftgpu has no CPU fallback)")
+        _TORCH = torch
+    return _TORCH
 
 
 def _stream_ptr(torch):
@@ -556,6 +564,14 @@ class TransformResult:  # include/sft/transforms.hpp:74-81
     kernel_rmse_percent: float
 
 
+def _host_ptr(a) -> int:
+    """Address of a host buffer (numpy array or CPU torch tensor) without building a
+    ctypes view: ndarray.ctypes costs microseconds per call on the streaming path."""
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.__array_interface__["data"][0]
+
+
 class TransformPlan:
     """Device plan: ``batch`` signals of ``n`` samples -> transform output, all in HBM.
     x: [batch][ld_x] (float32 for Single, float64 for Double); out: [batch][ld_out]
@@ -608,16 +624,15 @@ class TransformPlan:
     def execute_host(self, x_host: np.ndarray, out_host: np.ndarray, stream=None):
         torch = _torch()
         st = C.c_void_p(stream) if stream is not None else _stream_ptr(torch)
-        check(lib().sftgpu_transform_execute_host(self._h, x_host.ctypes.data_as(C.c_void_p),
-                                                  out_host.ctypes.data_as(C.c_void_p), st))
+        check(lib().sftgpu_transform_execute_host(self._h, C.c_void_p(_host_ptr(x_host)),
+                                                  C.c_void_p(_host_ptr(out_host)), st))
 
     def execute_host_async(self, x_host: np.ndarray, out_host: np.ndarray, stream=None):
         """Pipelined host-buffer execution (``sftgpu_transform_execute_host_async``): returns
         once queued; ``stream`` (default: torch's current) waits for the result copy."""
-        torch = _torch()
-        st = C.c_void_p(stream) if stream is not None else _stream_ptr(torch)
-        check(lib().sftgpu_transform_execute_host_async(self._h, x_host.ctypes.data_as(C.c_void_p),
-                                                        out_host.ctypes.data_as(C.c_void_p), st))
+        st = C.c_void_p(stream) if stream is not None else _stream_ptr(_torch())
+        check(lib().sftgpu_transform_execute_host_async(self._h, C.c_void_p(_host_ptr(x_host)),
+                                                        C.c_void_p(_host_ptr(out_host)), st))
 
     def synchronize(self):
         check(lib().sftgpu_plan_synchronize(self._h))
