@@ -106,3 +106,56 @@ def test_tc_rejects_ineligible_specs(sft):
     fp64 = sft.make_transform_spec("MDS5P6", 100.0, 10.0, sft.TransformOptions(precision=1))
     with pytest.raises(ValueError):
         sft.TransformPlan(fp64, 10000, 2, mode="tc")
+
+
+def test_tc_strided_and_unaligned_outputs(sft, O):
+    """Output layouts the TMA store cannot take: a padded row stride with count % 32 != 0,
+    and a row base offset by one complex element (8 bytes): K4 falls back to 16-byte /
+    element stores and matches the packed TMA result."""
+    import torch
+
+    spec = sft.make_transform_spec("MDS5P6", 600.0, 10.0, sft.TransformOptions(precision=0))
+    n, B = 30001, 3
+    xb = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 21, B, sft.Precision.Single)
+    plan = sft.TransformPlan(spec, n, B, mode="tc")
+    ref = plan.empty_output()
+    plan.execute(xb, ref)
+    ld = n + 7
+    big = torch.full((B * ld + 1, 2), float("nan"), dtype=torch.float32, device="cuda")
+    for off in (0, 1):
+        big.fill_(float("nan"))
+        view = big[off:off + B * ld].view(B, ld, 2)
+        plan.execute(xb, view, ld_out=ld)
+        torch.cuda.synchronize()
+        assert torch.equal(view[:, :n], ref)
+        assert torch.isnan(view[:, n:]).all()  # nothing written past count
+
+
+def test_tc_long_signal_chunks_match_cuda_core(sft, O):
+    """One long signal split into chunk items across the persistent CTAs (each chunk with
+    its own warm-up) equals K1's sequential result; first/last samples vs the oracle."""
+    import torch
+
+    spec = sft.make_transform_spec("MDS5P6", 3000.0, 10.0, sft.TransformOptions(precision=0))
+    n = 1 << 21
+    xb = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 5, 1, sft.Precision.Single)
+    plan, tc = _run(sft, spec, xb, "tc")
+    assert plan.describe()["chunks_per_signal"] > 1
+    _, k1 = _run(sft, spec, xb, "seq")
+    assert rel_max(tc, k1) < 1e-5
+    head = xb[0, :40000].double().cpu().numpy()
+    ref = oracle_transform(O, head, 1, spec)
+    # outputs far enough from the cut end are independent of the truncation
+    m = 40000 - 3 * 9100
+    assert rel_max(tc[0, :m], ref[:m]) < 1e-5
+
+
+def test_tc_batch_smaller_than_sms(sft, O):
+    """A few signals, each split into several chunk items (batch < 148)."""
+    spec = sft.make_transform_spec("MMS5P3", 1000.0, 10.0, sft.TransformOptions(precision=0))
+    n, B = 400000, 5
+    xb = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 8, B, sft.Precision.Single)
+    plan, tc = _run(sft, spec, xb, "tc")
+    assert plan.describe()["chunks_per_signal"] > 1
+    _, k1 = _run(sft, spec, xb, "seq")
+    assert rel_max(tc, k1) < 1e-5
