@@ -92,8 +92,15 @@ __device__ __forceinline__ double2 item_carry(const TcParams& P, long long item,
   return make_double2(v * P.g0[p].x, v * P.g0[p].y);
 }
 
+// Per-tile event clocks of CTA 0 for tools/tc_trace.py. Compiled in only with
+// -DTCK_TRACE=1 (SFTGPU_EXTRA_NVCC_FLAGS): the checks cost issue slots in every role.
+#ifndef TCK_TRACE
+#define TCK_TRACE 0
+#endif
 __device__ __forceinline__ void trace_ev(const TcParams& P, long long gt, int ev) {
-  if (P.trace && blockIdx.x == 0 && gt < 64) P.trace[gt * 16 + ev] = clock64();
+  if constexpr (TCK_TRACE) {
+    if (P.trace && blockIdx.x == 0 && gt < 64) P.trace[gt * 16 + ev] = clock64();
+  }
 }
 
 __device__ __forceinline__ float tf32_lo(float v) { return v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }

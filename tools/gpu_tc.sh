@@ -1,1 +1,2 @@
-timeout 300 python -m pytest tests/test_gpu_tc.py -x -q 2>&1 | tail -3
+timeout 300 python -m pytest tests/test_gpu_tc.py -x -q 2>&1 | tail -1
+timeout 300 python tools/tc_probe.py 2>&1 | tail -3

@@ -1,4 +1,6 @@
-"""Per-tile pipeline trace of K4 (CTA 0): clocks of loader issue / xfull, GEMM1 issue,
+"""Per-tile pipeline trace of K4 (CTA 0); needs a library built with the trace hooks:
+SFTGPU_EXTRA_NVCC_FLAGS="-DTCK_TRACE=1" python paper_2110_11866_b200/build.py
+(then rebuild without it). Columns: clocks: clocks of loader issue / xfull, GEMM1 issue,
 scan start / SS ready, GEMM2 issue, epilogue start / end, relative to the first event."""
 import sys, os, ctypes as C
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
