@@ -33,6 +33,8 @@ CASES = [
     ("MMS2P3", 64.0, 10.0, 9000, 5),
     ("GDS4P5", 512.0, 0.0, 50000, 2),
     ("MDP6", 1000.0, 10.0, 30000, 2),      # SFT (alpha = 0)
+    ("GDP6", 4000.0, 0.0, 102400, 2),      # Gaussian SFT, real output
+    ("MMS1P2", 20.0, 12.0, 40000, 7),      # tiny sigma: one warm-up tile
 ]
 
 
@@ -47,6 +49,20 @@ def test_tc_vs_oracle_and_cuda_core(sft, O, abbrev, sigma, xi, n, batch):
     for b in sorted({0, batch - 1}):
         assert rel_max(tc[b], oracle_transform(O, xh[b], 1, spec)) < 1e-5
     assert rel_max(tc, ref1) < 1e-5
+
+
+@pytest.mark.parametrize("gkind,n0", [(1, 0), (1, 5), (2, 0), (2, 5)])
+def test_tc_gaussian_derivatives(sft, O, gkind, n0):
+    """First / second Gaussian derivatives (proj/src/transforms.cpp:279-335 weights on the
+    sin / cos components, plus the ASFT corrections for n0 > 0) on K4."""
+    spec = sft.make_gauss_spec(700.0, gkind, 6, n0, sft.TransformOptions(precision=0))
+    n, batch = 40000, 2
+    xb = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 13, batch, sft.Precision.Single)
+    _, tc = _run(sft, spec, xb, "tc")
+    _, k1 = _run(sft, spec, xb, "seq")
+    xh = xb.double().cpu().numpy()
+    assert rel_max(tc[1], oracle_transform(O, xh[1], 1, spec)) < 1e-5
+    assert rel_max(tc, k1) < 1e-5
 
 
 @pytest.mark.parametrize("boundary", [0, 1])

@@ -1,1 +1,1 @@
-for w in gauss_asft_fp32 morlet_direct; do timeout 300 python bench.py --no-cpu --workload $w 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['workload'], d['ms_per_step']*1e3, 'us', d['e2e']['value'])"; done
+timeout 300 python -m pytest tests/test_gpu_tc.py -x -q 2>&1 | tail -2
