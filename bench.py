@@ -344,7 +344,7 @@ def run_ours(args, w, spec_of):
     e2e_value = n * batch * e2e_steps * world / max_over_ranks(e2e_s, world) / 1e6
     e2e_path = ("sftgpu_transform_execute_host_async (C ABI, pipelined over 3 pinned host buffer pairs; "
                 "wall clock around all steps + final stream sync)" if pairs > 1 else
-                "sftgpu_transform_execute_host (C ABI, pinned host buffers, synchronous per step)")
+                "sftgpu_transform_execute_host (C ABI, pinned host buffers, one synchronous call per step; large tensor-core plans pipeline sub-batches inside the call)")
 
     peak, peak_src = measured_peaks()
     launches = plan.launches

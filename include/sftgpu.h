@@ -237,7 +237,10 @@ int sftgpu_transform_plan_create_ex(const sftgpu_spec* spec, int64_t n, int64_t 
 int sftgpu_transform_execute(sftgpu_plan* plan, const void* x, int64_t ld_x, void* out,
                              int64_t ld_out, void* stream);
 /* Same, from/to HOST memory of the plan's precision (host<->device copies included;
- * pinned memory recommended). Synchronises `stream` before returning. */
+ * pinned memory recommended). Synchronises `stream` before returning. Large tensor-core
+ * (K4) plans pipeline sub-batches of signals through the plan's copy-in / compute /
+ * copy-out streams inside the call, so the copies of one sub-batch overlap the kernel
+ * of the next. */
 int sftgpu_transform_execute_host(sftgpu_plan* plan, const void* x_host, void* out_host,
                                   void* stream);
 /* Pipelined variant for streams of host buffers: enqueues H2D of x_host, the transform

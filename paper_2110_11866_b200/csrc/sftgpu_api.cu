@@ -146,6 +146,10 @@ struct sftgpu_plan {
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
   cudaEvent_t ev_entry = nullptr;
   int next_slot = 0;
+  // sub-batched synchronous host execution (large K4 plans): two device staging slots
+  void* sb_x[2] = {nullptr, nullptr};
+  void* sb_out[2] = {nullptr, nullptr};
+  size_t sb_cap_x[2] = {0, 0}, sb_cap_out[2] = {0, 0};
 
   ~sftgpu_plan() {
     if (s_in) {
@@ -167,6 +171,10 @@ struct sftgpu_plan {
     for (Group& g : groups) {
       cudaFree(g.d_tab);
       cudaFree(g.d_tab_tile);
+    }
+    for (int k = 0; k < 2; ++k) {
+      cudaFree(sb_x[k]);
+      cudaFree(sb_out[k]);
     }
     cudaFree(d_tc_image);
     cudaFree(d_ctrl);
@@ -876,7 +884,7 @@ EncodeTiledFn encode_tiled() {
   return fn;
 }
 
-bool make_out_map(sftgpu_plan* pl, void* out, long long ld_out, CUtensorMap* map) {
+bool make_out_map(sftgpu_plan* pl, void* out, long long ld_out, long long nsig, CUtensorMap* map) {
   const tck::TcParams& P = pl->tcp;
   const int cw = P.cplx ? 2 : 1;
   if (pl->count % tck::kQ != 0 || reinterpret_cast<uintptr_t>(out) % 16 != 0) return false;
@@ -887,13 +895,13 @@ bool make_out_map(sftgpu_plan* pl, void* out, long long ld_out, CUtensorMap* map
   const cuuint64_t sig_stride = static_cast<cuuint64_t>(ld_out) * cw * sizeof(float);
   CUresult r;
   if (cw == 2) {
-    const cuuint64_t dims[4] = {32, 2, rows, static_cast<cuuint64_t>(pl->batch)};
+    const cuuint64_t dims[4] = {32, 2, rows, static_cast<cuuint64_t>(nsig)};
     const cuuint64_t strides[3] = {128, 256, sig_stride};
     const cuuint32_t box[4] = {32, 1, 128, 1}, es[4] = {1, 1, 1, 1};
     r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
-    const cuuint64_t dims[3] = {32, rows, static_cast<cuuint64_t>(pl->batch)};
+    const cuuint64_t dims[3] = {32, rows, static_cast<cuuint64_t>(nsig)};
     const cuuint64_t strides[2] = {128, sig_stride};
     const cuuint32_t box[3] = {32, 128, 1}, es[3] = {1, 1, 1};
     r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -904,14 +912,24 @@ bool make_out_map(sftgpu_plan* pl, void* out, long long ld_out, CUtensorMap* map
 
 long long* g_tc_trace = nullptr;  // diagnostics: sftgpu_debug_set_tc_trace
 
-void run_tc(sftgpu_plan* pl, const void* x, long long ld_x, void* out, long long ld_out, cudaStream_t st) {
+// K4 over the plan's signals, or over the first `nsig` signals at x / out (sub-batches of
+// the pipelined host path: same geometry, fewer items)
+void run_tc(sftgpu_plan* pl, const void* x, long long ld_x, void* out, long long ld_out, cudaStream_t st,
+            long long nsig = -1) {
   tck::TcParams& C = pl->tcp;
-  if (pl->tc_map_out != out || pl->tc_map_ld != ld_out) {
-    C.use_tma = make_out_map(pl, out, ld_out, &C.out_map) ? 1 : 0;
-    pl->tc_map_out = out;
-    pl->tc_map_ld = ld_out;
+  tck::TcParams P;
+  if (nsig < 0 || nsig == pl->batch) {
+    if (pl->tc_map_out != out || pl->tc_map_ld != ld_out) {
+      C.use_tma = make_out_map(pl, out, ld_out, pl->batch, &C.out_map) ? 1 : 0;
+      pl->tc_map_out = out;
+      pl->tc_map_ld = ld_out;
+    }
+    P = C;
+  } else {
+    P = C;
+    P.n_items = nsig * C.n_chunks;
+    P.use_tma = make_out_map(pl, out, ld_out, nsig, &P.out_map) ? 1 : 0;
   }
-  tck::TcParams P = C;
   P.x = static_cast<const float*>(x);
   P.out = static_cast<float*>(out);
   P.ld_x = ld_x;
@@ -920,7 +938,8 @@ void run_tc(sftgpu_plan* pl, const void* x, long long ld_x, void* out, long long
   P.vec_ok = (reinterpret_cast<uintptr_t>(out) % 16 == 0 && rowb % 16 == 0) ? 1 : 0;
   if (const char* e = std::getenv("SFTGPU_TC_NO_TMA")) P.use_tma = e[0] == '1' ? 0 : P.use_tma;
   P.trace = g_tc_trace;
-  cuda_check(tck::launch_tc(P, pl->tc_grid, st), "sft_tc_kernel launch");
+  const int grid = static_cast<int>(std::min<long long>(pl->tc_grid, P.n_items));
+  cuda_check(tck::launch_tc(P, grid, st), "sft_tc_kernel launch");
 }
 
 template <typename T>
@@ -1316,11 +1335,67 @@ void run_transform(sftgpu_plan* pl, const void* d_x, void* d_out, cudaStream_t s
 }
 }  // namespace
 
+namespace {
+void ensure_pipeline(sftgpu_plan* pl) {
+  if (pl->s_in) return;
+  const unsigned fl = cudaStreamNonBlocking;
+  cuda_check(cudaStreamCreateWithFlags(&pl->s_in, fl), "stream create");
+  cuda_check(cudaStreamCreateWithFlags(&pl->s_comp, fl), "stream create");
+  cuda_check(cudaStreamCreateWithFlags(&pl->s_out, fl), "stream create");
+  cuda_check(cudaEventCreateWithFlags(&pl->ev_entry, cudaEventDisableTiming), "event create");
+  for (auto& sl : pl->slots) {
+    cuda_check(cudaEventCreateWithFlags(&sl.ev_in, cudaEventDisableTiming), "event create");
+    cuda_check(cudaEventCreateWithFlags(&sl.ev_comp, cudaEventDisableTiming), "event create");
+    cuda_check(cudaEventCreateWithFlags(&sl.ev_out, cudaEventDisableTiming), "event create");
+  }
+}
+
+// Large K4 plans from host memory: sub-batches of signals flow through two device staging
+// slots on the copy-in / compute / copy-out streams, so H2D of sub-batch k+1, the kernel
+// of k and D2H of k-1 overlap (the whole-batch copies are otherwise serial).
+void execute_host_subbatched(sftgpu_plan* pl, const void* x_host, void* out_host, cudaStream_t user) {
+  ensure_pipeline(pl);
+  const long long parts = std::min<long long>(8, pl->batch);
+  const long long sub = (pl->batch + parts - 1) / parts;
+  const size_t es = sizeof(float), cw = pl->mode == sftk::kModeComplex ? 2 : 1;
+  const size_t xsig = static_cast<size_t>(pl->n) * es, osig = static_cast<size_t>(pl->count) * cw * es;
+  for (int k = 0; k < 2; ++k) {
+    ensure_buffer(&pl->sb_x[k], &pl->sb_cap_x[k], sub * xsig, "cudaMalloc sub-batch x");
+    ensure_buffer(&pl->sb_out[k], &pl->sb_cap_out[k], sub * osig, "cudaMalloc sub-batch out");
+  }
+  cuda_check(cudaEventRecord(pl->ev_entry, user), "event record");
+  cuda_check(cudaStreamWaitEvent(pl->s_in, pl->ev_entry, 0), "stream wait");
+  for (long long k = 0; k * sub < pl->batch; ++k) {
+    const long long s0 = k * sub, ns = std::min(sub, pl->batch - s0);
+    auto& sl = pl->slots[k & 1];
+    if (k >= 2) cuda_check(cudaStreamWaitEvent(pl->s_in, sl.ev_comp, 0), "stream wait");
+    cuda_check(cudaMemcpyAsync(pl->sb_x[k & 1], static_cast<const char*>(x_host) + s0 * xsig, ns * xsig,
+                               cudaMemcpyHostToDevice, pl->s_in),
+               "H2D");
+    cuda_check(cudaEventRecord(sl.ev_in, pl->s_in), "event record");
+    cuda_check(cudaStreamWaitEvent(pl->s_comp, sl.ev_in, 0), "stream wait");
+    if (k >= 2) cuda_check(cudaStreamWaitEvent(pl->s_comp, sl.ev_out, 0), "stream wait");
+    run_tc(pl, pl->sb_x[k & 1], pl->n, pl->sb_out[k & 1], pl->count, pl->s_comp, ns);
+    cuda_check(cudaEventRecord(sl.ev_comp, pl->s_comp), "event record");
+    cuda_check(cudaStreamWaitEvent(pl->s_out, sl.ev_comp, 0), "stream wait");
+    cuda_check(cudaMemcpyAsync(static_cast<char*>(out_host) + s0 * osig, pl->sb_out[k & 1], ns * osig,
+                               cudaMemcpyDeviceToHost, pl->s_out),
+               "D2H");
+    cuda_check(cudaEventRecord(sl.ev_out, pl->s_out), "event record");
+  }
+  cuda_check(cudaStreamSynchronize(pl->s_out), "stream sync");
+}
+}  // namespace
+
 int sftgpu_transform_execute_host(sftgpu_plan* pl, const void* x_host, void* out_host, void* stream) {
   return guarded([&] {
     if (!pl || pl->is_components) fail(SFTGPU_EINVAL, "not a transform plan");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t xb = plan_in_bytes(pl), ob = plan_out_bytes(pl);
+    if (pl->tc && pl->batch >= 4 && xb + ob >= (256u << 20)) {
+      execute_host_subbatched(pl, x_host, out_host, st);
+      return;
+    }
     ensure_buffer(&pl->d_x, &pl->cap_x, xb, "cudaMalloc staging x");
     ensure_buffer(&pl->d_out, &pl->cap_out, ob, "cudaMalloc staging out");
     cuda_check(cudaMemcpyAsync(pl->d_x, x_host, xb, cudaMemcpyHostToDevice, st), "H2D");
@@ -1335,18 +1410,7 @@ int sftgpu_transform_execute_host_async(sftgpu_plan* pl, const void* x_host, voi
     if (!pl || pl->is_components) fail(SFTGPU_EINVAL, "not a transform plan");
     if (!x_host || !out_host) fail(SFTGPU_EINVAL, "null host buffer");
     cudaStream_t user = static_cast<cudaStream_t>(stream);
-    if (!pl->s_in) {
-      const unsigned fl = cudaStreamNonBlocking;
-      cuda_check(cudaStreamCreateWithFlags(&pl->s_in, fl), "stream create");
-      cuda_check(cudaStreamCreateWithFlags(&pl->s_comp, fl), "stream create");
-      cuda_check(cudaStreamCreateWithFlags(&pl->s_out, fl), "stream create");
-      cuda_check(cudaEventCreateWithFlags(&pl->ev_entry, cudaEventDisableTiming), "event create");
-      for (auto& sl : pl->slots) {
-        cuda_check(cudaEventCreateWithFlags(&sl.ev_in, cudaEventDisableTiming), "event create");
-        cuda_check(cudaEventCreateWithFlags(&sl.ev_comp, cudaEventDisableTiming), "event create");
-        cuda_check(cudaEventCreateWithFlags(&sl.ev_out, cudaEventDisableTiming), "event create");
-      }
-    }
+    ensure_pipeline(pl);
     const size_t xb = plan_in_bytes(pl), ob = plan_out_bytes(pl);
     auto& sl = pl->slots[pl->next_slot];
     pl->next_slot = (pl->next_slot + 1) % sftgpu_plan::kSlots;

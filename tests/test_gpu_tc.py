@@ -175,3 +175,23 @@ def test_tc_batch_smaller_than_sms(sft, O):
     assert plan.describe()["chunks_per_signal"] > 1
     _, k1 = _run(sft, spec, xb, "seq")
     assert rel_max(tc, k1) < 1e-5
+
+
+def test_tc_subbatched_host_execution(sft, O):
+    """sftgpu_transform_execute_host on a large K4 plan pipelines sub-batches of signals
+    through two device staging slots (H2D / kernel / D2H overlap): the result equals the
+    device-buffer execution bit for bit."""
+    import torch
+
+    spec = sft.make_transform_spec("MMS5P3", 300.0, 10.0, sft.TransformOptions(precision=0))
+    n, B = 102400, 250  # 307 MB of host input + output: above the sub-batching threshold
+    xb = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 17, B, sft.Precision.Single)
+    plan = sft.TransformPlan(spec, n, B)
+    assert plan.describe()["tensor_cores"] == 1
+    ref = plan.empty_output()
+    plan.execute(xb, ref)
+    torch.cuda.synchronize()
+    xh = xb.cpu().numpy()
+    oh = np.empty(tuple(ref.shape), dtype=np.float32)
+    plan.execute_host(xh, oh)
+    assert np.array_equal(oh, ref.cpu().numpy())
