@@ -43,6 +43,7 @@ namespace sftk {
 constexpr int kMaxOrd = 12;
 constexpr int kMaxL = 16;
 constexpr int kTabStride = 64;  // table entries per order (see layout below)
+constexpr int kTabTileStride = 6;  // tile-table entries per order
 
 enum Mode { kModeReal = 0, kModeComplex = 1, kModeComps = 2 };
 // Injection group modes: 0 one real constant for all orders, 1 split (first NA orders
@@ -85,7 +86,9 @@ struct OrdConst {
 //   [32, 37)  z^{L*2^k}      warp-scan multipliers
 //   [40, 56)  z^{32L*w}      per-warp carry rotation, w < NW
 //   [56, 60)  z^{32L*2^k}    inter-warp scan multipliers
-// Tile table (double2, per order): [0] z^{TT}, [1] z^{32 TT}.
+// Tile table (double2, per order, stride kTabTileStride): [0] z^{TT}, [1] z^{32 TT},
+// [2 + g] z^{TT (cnt - min(cnt, (g + 1) ceil(cnt / G)))}: the LB window-carry segment
+// scales (cnt = D + 1 predecessors, G = 4 lane groups for <= 8 orders, else 2).
 template <typename T>
 struct ScanParams {
   const T* x;
@@ -118,17 +121,17 @@ struct ScanParams {
   double2* incl;
   const T* tab;  // [NORD][kTabStride][4] entries {re, re, -im, im}
   const double2* tab_tile;
+  long long* trace;  // optional LB phase timestamps ([tile][8] globaltimer ns), tools/scan_trace.py
   T cAr, cAi, cBr, cBi;  // shared injection constants (group modes 0/1)
   T Dr, Di;
   OrdConst<T> oc[kMaxOrd];
 };
 
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-
 __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -243,6 +246,23 @@ struct Smem {
   unsigned int epoch;
 };
 
+// LB phase timestamps for tools/scan_trace.py, compiled in only with -DSFTK_TRACE=1
+// (SFTGPU_EXTRA_NVCC_FLAGS): 0 entry, 1 ticket, 2 staged, 3 published, 4 carry, 5 done,
+// 6 lead-only sums, 7 window-carry start.
+#ifndef SFTK_TRACE
+#define SFTK_TRACE 0
+#endif
+template <typename T>
+__device__ __forceinline__ void trace_ev(const ScanParams<T>& P, long long gt, int ev) {
+  if constexpr (SFTK_TRACE) {
+    if (P.trace && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      P.trace[gt * 8 + ev] = static_cast<long long>(t);
+    }
+  }
+}
+
 // LB-mode carry (warp 0). The window state depends only on the last 2K leading
 // samples, V[n] = sum_{m=n-2K+1}^{n} z^{n-m} x[m+K], so the carry into tile t is the
 // finite sum  sum_{d=1}^{D} z^{TT(d-1)} LA_{t-d} + z^{TT D} SA_{t-D-1}  of the
@@ -254,31 +274,69 @@ template <typename T, int NORD, int L, int NT, bool SEQ>
 __device__ __forceinline__ void window_carry(const ScanParams<T>& P, Smem<T, NORD, L, NT, SEQ>& S, long long gt,
                                              long long first, int lane) {
   double2 acc = make_double2(0.0, 0.0);
-  const double2 zT = lane < NORD ? P.tab_tile[lane * 2] : make_double2(1.0, 0.0);
+  const double2 zT = lane < NORD ? P.tab_tile[lane * kTabTileStride] : make_double2(1.0, 0.0);
   for (int hi = P.lb_D + 1; hi >= 1; hi -= 64) {
     const int lo_d = hi - 63 > 1 ? hi - 63 : 1;
     const int cnt = hi - lo_d + 1;
+    // Each lane stages predecessors j = lane and lane + 32 in two round trips: both
+    // flags polled together (relaxed), one acquire fence, then both payloads in flight
+    // together (a poll + payload pair per predecessor would be four).
+    const unsigned int ep = S.epoch;
+    long long t[2];
+    bool live[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int j = lane + 32 * k;
-      if (j < cnt) {
-        const int d = hi - j;
-        const long long t = gt - d;
-        if (t < first) {
-#pragma unroll
-          for (int p = 0; p < NORD; ++p) S.pay[j][p] = make_double2(0.0, 0.0);
-        } else {
-          while ((static_cast<unsigned int>(ld_acquire_u64(P.flags + t) >> 32)) != S.epoch) {
-          }
-          const double2* src = (d == P.lb_D + 1) ? P.incl : P.agg;
-#pragma unroll
-          for (int p = 0; p < NORD; ++p) S.pay[j][p] = __ldcg(src + t * NORD + p);
-        }
-      }
+      t[k] = gt - (hi - j);
+      live[k] = j < cnt && t[k] >= first;
     }
+    unsigned long long f[2] = {0ull, 0ull};
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (live[k]) f[k] = ld_relaxed_u64(P.flags + t[k]);
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (live[k])
+        while (static_cast<unsigned int>(f[k] >> 32) != ep) f[k] = ld_relaxed_u64(P.flags + t[k]);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    double2 v[2][NORD];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double2* src = (hi - (lane + 32 * k) == P.lb_D + 1) ? P.incl : P.agg;
+#pragma unroll
+      for (int p = 0; p < NORD; ++p) v[k][p] = live[k] ? __ldcg(src + t[k] * NORD + p) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (lane + 32 * k < cnt) {
+#pragma unroll
+        for (int p = 0; p < NORD; ++p) S.pay[lane + 32 * k][p] = v[k][p];
+      }
     __syncwarp();
-    if (lane < NORD)
+    if (hi == P.lb_D + 1 && hi <= 64) {
+      // Single round (the common case, D + 1 <= 64): G lane groups each Horner one
+      // segment of the predecessors and scale it by z^{TT (cnt - segment end)} (host
+      // table), then the groups are summed with shuffles: the fp64 dependency chain is
+      // cnt / G long instead of cnt.
+      constexpr int G = NORD <= 8 ? 4 : 2, WG = 32 / G;
+      const int g = lane / WG, p = lane % WG;
+      const int seg = (cnt + G - 1) / G;
+      const int j0 = g * seg, j1 = min(cnt, j0 + seg);
+      double2 part = make_double2(0.0, 0.0);
+      if (p < NORD) {
+        const double2 zp = P.tab_tile[p * kTabTileStride];
+        for (int j = j0; j < j1; ++j) part = cadd(cmul(part, zp), S.pay[j][p]);
+        part = cmul(part, P.tab_tile[p * kTabTileStride + 2 + g]);
+      }
+#pragma unroll
+      for (int off = WG; off < 32; off <<= 1) {
+        part.x += __shfl_xor_sync(0xffffffffu, part.x, off);
+        part.y += __shfl_xor_sync(0xffffffffu, part.y, off);
+      }
+      acc = part;
+    } else if (lane < NORD) {
       for (int j = 0; j < cnt; ++j) acc = cadd(cmul(acc, zT), S.pay[j][lane]);
+    }
     __syncwarp();
   }
   if (lane < NORD) S.carry[lane] = acc;
@@ -495,6 +553,7 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
 
   if constexpr (SEQ) cp_async_wait_all();
   __syncthreads();  // this tile staged; the other buffer's last readers are done
+  if constexpr (!SEQ) trace_ev(P, gt, 2);
   if constexpr (SEQ) {
     if (has_next) stage_tile<T, L, NT, true>(P, xs, lo, o0 + TT, tid, S.lead[b ^ 1], S.trail[b ^ 1]);
   }
@@ -513,7 +572,7 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
         la = X::agg_r(c, i, xl, la);
         sa = X::agg_r(c, i, e >= P.lb_sfx ? xl : T(0), sa);
       }
-      const T* rot = P.tab + (p * kTabStride + 31 - lane) * 4;  // z^{L(31-lane)}
+      const T* rot = P.tab + (p * kTabStride + 31 - lane) * 4;  // z^{L(31-lane)} (prefetched)
       la = X::warp_sum(X::madd(rot, la, X::zero()));
       sa = X::warp_sum(X::madd(rot, sa, X::zero()));
       if (lane == 0) {
@@ -521,6 +580,7 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
         S.wsa[warp][p] = make2<T2>(X::re(sa), X::im(sa));
       }
     }
+    trace_ev(P, gt, 6);
     __syncthreads();
     if (tid < NORD) {
       const int p = tid;
@@ -543,8 +603,12 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
         }
         st_release_u64(P.flags + gt, (static_cast<unsigned long long>(S.epoch) << 32) | 1ull);
       }
+      trace_ev(P, gt, 3);
     }
-    if (warm) return;  // warm tiles only feed their successors' windows
+    if (warm) {
+      trace_ev(P, gt, 5);
+      return;  // warm tiles only feed their successors' windows
+    }
   }
 
   // ---- injections, shared across orders where the group mode allows. Samples are
@@ -651,7 +715,7 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
         const St r = X::madd(P.oc[p].wrot[w], cs, ex[w]);
         S.w[w][p] = make2<T2>(X::re(r), X::im(r));
       }
-      S.carry[p] = cadd(cmul(P.tab_tile[p * 2], c), S.tagg[p]);
+      S.carry[p] = cadd(cmul(P.tab_tile[p * kTabTileStride], c), S.tagg[p]);
     } else {
 #pragma unroll
       for (int w = 0; w < NW; ++w) S.w[w][p] = make2<T2>(X::re(ex[w]), X::im(ex[w]));
@@ -660,7 +724,9 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
   if constexpr (!SEQ) {
     if (warp == 0) {
       __syncwarp();
+      trace_ev(P, gt, 7);
       window_carry<T, NORD, L, NT, SEQ>(P, S, gt, first, lane);
+      trace_ev(P, gt, 4);
       if (tid < NORD) {
         const int p = tid;
 
@@ -786,13 +852,49 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? (L >= 16 ? 5 : (N
   extern __shared__ __align__(16) unsigned char smem_raw[];  // sized by the launcher
   Smem<T, NORD, L, NT, SEQ>& S = *reinterpret_cast<Smem<T, NORD, L, NT, SEQ>*>(smem_raw);
   const int tid = threadIdx.x;
+  // LB: the ticket's round trip overlaps the table staging below (consumed after it)
+  // and the epoch read. The epoch only changes when this launch's last CTA re-arms the
+  // control block, after every CTA has counted in (after its ticket), so it can be read
+  // alongside the ticket.
+  unsigned int ticket = 0, epoch = 0;
+  unsigned long long t_entry = 0;
+  if constexpr (!SEQ) {
+    if constexpr (SFTK_TRACE) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
+    if (tid == 0) {
+      epoch = *reinterpret_cast<volatile unsigned int*>(P.ctrl + 2);
+      ticket = atomicAdd(P.ctrl, 1u);
+    }
+  }
+  if constexpr (!SEQ) {
+    // tables read later on the tile's chain (lead-only warp sums, window carry): start
+    // their fetch now, without waiting on it
+    // (one warp: every CTA of the launch reads the same few table lines at once)
+    if (tid < 32) {
+#pragma unroll
+      for (int p = 0; p < NORD; ++p)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(P.tab + (p * kTabStride + 31 - tid) * 4));
+      if (tid < NORD) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.tab_tile + tid * kTabTileStride));
+    }
+  }
   {
+    // every load issued before the first store (one round trip, not one per element)
     using Sm = Smem<T, NORD, L, NT, SEQ>;
     constexpr int E = Sm::SEG + Sm::SEGS;
-    for (int q = tid; q < NORD * E * 4; q += NT) {
-      const int p = q / (E * 4), j = (q / 4) % E, w = q % 4;
-      const int src = j < Sm::SEG ? j : Sm::SEG * (j - Sm::SEG);
-      S.ptab[p][j][w] = P.tab[(p * kTabStride + src) * 4 + w];
+    constexpr int NQ = (NORD * E * 4 + NT - 1) / NT;
+    T v[NQ];
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      const int q = tid + k * NT;
+      if (q < NORD * E * 4) {
+        const int p = q / (E * 4), j = (q / 4) % E, w = q % 4;
+        const int src = j < Sm::SEG ? j : Sm::SEG * (j - Sm::SEG);
+        v[k] = P.tab[(p * kTabStride + src) * 4 + w];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      const int q = tid + k * NT;
+      if (q < NORD * E * 4) (&S.ptab[0][0][0])[q] = v[k];
     }
   }
 
@@ -815,24 +917,32 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? (L >= 16 ? 5 : (N
                                                   t + 1 < tiles);
   } else {
     if (tid == 0) {
-      S.tile = static_cast<long long>(atomicAdd(P.ctrl, 1u));
-      S.epoch = *reinterpret_cast<volatile unsigned int*>(P.ctrl + 2);
-      // every CTA has its ticket once the count is complete: the last one re-arms the
-      // control block (the next launch is stream-ordered after this one)
-      if (atomicAdd(P.ctrl + 1, 1u) == static_cast<unsigned int>(P.total_tiles - 1)) {
-        atomicExch(P.ctrl, 0u);
-        atomicExch(P.ctrl + 1, 0u);
-        atomicAdd(P.ctrl + 2, 1u);
-      }
+      S.tile = static_cast<long long>(ticket);
+      S.epoch = epoch;
     }
     __syncthreads();
+    // count in (after the ticket); inspected once this tile's loads are in flight. Every
+    // CTA has its ticket once the count is complete: the last one re-arms the control
+    // block (the next launch is stream-ordered after this one).
+    unsigned int counted = 0;
+    if (tid == 0) counted = atomicAdd(P.ctrl + 1, 1u);
     const long long gt = S.tile;
+    if constexpr (SFTK_TRACE) {
+      if (P.trace && tid == 0) P.trace[gt * 8] = static_cast<long long>(t_entry);
+    }
+    trace_ev(P, gt, 1);
     const long long sig = gt / P.tiles_per_signal;
     const long long first = sig * P.tiles_per_signal;
     const long long o0 = (gt - first - P.warm_tiles) * TT;
     const T* __restrict__ xs = P.x + sig * P.ld_x;
     stage_tile<T, L, NT, false>(P, xs, P.lo, o0, tid, S.lead[0], S.trail[0]);
+    if (tid == 0 && counted == static_cast<unsigned int>(P.total_tiles - 1)) {
+      atomicExch(P.ctrl, 0u);
+      atomicExch(P.ctrl + 1, 0u);
+      atomicAdd(P.ctrl + 2, 1u);
+    }
     do_tile<T, NORD, NA, GM, MODE, L, NT, false>(P, S, sig, gt, first, P.lo, P.count, 0, o0, xs, false);
+    if (o0 + TT > 0) trace_ev(P, gt, 5);
   }
 }
 

@@ -312,11 +312,14 @@ void fill_consts(sftk::ScanParams<T>& P, const std::vector<Order>& ords, double 
 }
 
 template <typename T>
-void build_tables(Group& g, const std::vector<Order>& ords, double alpha, int L, int NT) {
+void build_tables(Group& g, const std::vector<Order>& ords, double alpha, int L, int NT, int K) {
   const int NW = NT / 32;
   const long long TT = static_cast<long long>(L) * NT;
   std::vector<T> tab(static_cast<size_t>(ords.size()) * sftk::kTabStride * 4, T(0));
-  std::vector<double2> tt(static_cast<size_t>(ords.size()) * 2);
+  std::vector<double2> tt(static_cast<size_t>(ords.size()) * sftk::kTabTileStride);
+  const long long cnt = (2LL * K) / TT + 1;  // LB window-carry predecessors (lb_D + 1)
+  const int G = ords.size() <= 8 ? 4 : 2;
+  const long long seg = (cnt + G - 1) / G;
   auto put = [](T* d, cd v) {  // {re, re, -im, im}
     d[0] = static_cast<T>(v.real());
     d[1] = static_cast<T>(v.real());
@@ -332,7 +335,12 @@ void build_tables(Group& g, const std::vector<Order>& ords, double alpha, int L,
     for (int k = 0; k < 4; ++k) put(t + (56 + k) * 4, zpow(alpha, w, 32.0 * L * (1 << k)));
     for (int l = 0; l < 2; ++l) {
       const cd v = zpow(alpha, w, static_cast<double>(TT) * (l == 0 ? 1 : 32));
-      tt[p * 2 + l] = make_double2(v.real(), v.imag());
+      tt[p * sftk::kTabTileStride + l] = make_double2(v.real(), v.imag());
+    }
+    for (int gi = 0; gi < 4; ++gi) {
+      const long long e = cnt - std::min(cnt, (gi + 1) * seg);
+      const cd v = zpow(alpha, w, static_cast<double>(TT) * static_cast<double>(e));
+      tt[p * sftk::kTabTileStride + 2 + gi] = make_double2(v.real(), v.imag());
     }
   }
   cuda_check(cudaMalloc(&g.d_tab, tab.size() * sizeof(T)), "cudaMalloc tables");
@@ -391,7 +399,7 @@ void build_groups(sftgpu_plan* pl, std::vector<Order> ords, double alpha, double
     // each launch adds its own orders' share of the x[n-K] term
     P.Dr = static_cast<T>(Dr);
     P.Di = static_cast<T>(Di);
-    build_tables<T>(g, sub, alpha, pl->L, pl->NT);
+    build_tables<T>(g, sub, alpha, pl->L, pl->NT, pl->K);
     P.tab = static_cast<const T*>(g.d_tab);
     P.tab_tile = g.d_tab_tile;
   }
@@ -910,7 +918,8 @@ bool make_out_map(sftgpu_plan* pl, void* out, long long ld_out, long long nsig, 
   return r == CUDA_SUCCESS;
 }
 
-long long* g_tc_trace = nullptr;  // diagnostics: sftgpu_debug_set_tc_trace
+long long* g_tc_trace = nullptr;    // diagnostics: sftgpu_debug_set_tc_trace
+long long* g_scan_trace = nullptr;  // diagnostics: sftgpu_debug_set_scan_trace
 
 // K4 over the plan's signals, or over the first `nsig` signals at x / out (sub-batches of
 // the pipelined host path: same geometry, fewer items)
@@ -979,6 +988,7 @@ void run_groups(sftgpu_plan* pl, const void* x, long long ld_x, void* out, void*
       P.lb_sfx = static_cast<int>(pl->TT - r);
     }
     P.ctrl = pl->d_ctrl;
+    P.trace = g_scan_trace;
     P.flags = pl->d_flags;
     P.agg = pl->d_agg;
     P.incl = pl->d_incl;
@@ -1525,6 +1535,9 @@ void sftgpu_plan_destroy(sftgpu_plan* pl) { delete pl; }
 /* Diagnostics (not part of the reference interface): device buffer of 64 x 16 int64 that
  * K4 fills with per-tile event clocks of CTA 0 (tools/tc_trace.py); NULL disables. */
 void sftgpu_debug_set_tc_trace(void* dev_buf) { g_tc_trace = static_cast<long long*>(dev_buf); }
+/* Diagnostics: device buffer of tiles x 8 int64 that K1 LB fills with per-tile phase
+ * timestamps when built with -DSFTK_TRACE=1 (tools/scan_trace.py); NULL disables. */
+void sftgpu_debug_set_scan_trace(void* dev_buf) { g_scan_trace = static_cast<long long*>(dev_buf); }
 
 int sftgpu_generate_signal(int kind, int64_t n, uint64_t seed, int64_t batch, int dtype, void* out, void* stream) {
   return guarded([&] {
