@@ -132,6 +132,24 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// fp32 plans publish look-back payloads without flags: every 8-byte word carries a launch
+// tag in its low 4 bits. The payload doubles are converted from fp32, so those bits are
+// zero and stripping the tag restores them exactly; each aligned 8-byte word is
+// single-copy atomic, so a reader that sees the current tag sees that word's value
+// (no release fence on the producer, no flag round trip on the consumer).
+__device__ __forceinline__ unsigned long long pay_tag(unsigned int epoch) { return (epoch % 15u) + 1u; }
+__device__ __forceinline__ unsigned long long tag_word(double v, unsigned long long tg) {
+  return (static_cast<unsigned long long>(__double_as_longlong(v)) & ~15ull) | tg;
+}
+__device__ __forceinline__ double untag_word(unsigned long long w) {
+  return __longlong_as_double(static_cast<long long>(w & ~15ull));
+}
+__device__ __forceinline__ void st_relaxed_v2(double2* p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_relaxed_v2(const double2* p, unsigned long long& a, unsigned long long& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
 __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -290,28 +308,68 @@ __device__ __forceinline__ void window_carry(const ScanParams<T>& P, Smem<T, NOR
       t[k] = gt - (hi - j);
       live[k] = j < cnt && t[k] >= first;
     }
-    unsigned long long f[2] = {0ull, 0ull};
+    if constexpr (sizeof(T) == 4) {
+      // tagged payloads: one round trip when the predecessors have published
+      const unsigned long long tg = pay_tag(ep);
+      constexpr int KB = NORD <= 8 ? 2 : 1;  // predecessors in flight per lane (registers)
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
-      if (live[k]) f[k] = ld_relaxed_u64(P.flags + t[k]);
+      for (int k0 = 0; k0 < 2; k0 += KB) {
+        unsigned long long w[KB][NORD][2];
+        auto load = [&](int kk) {
+          const int k = k0 + kk;
+          const double2* src = ((hi - (lane + 32 * k) == P.lb_D + 1) ? P.incl : P.agg) + t[k] * NORD;
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
-      if (live[k])
-        while (static_cast<unsigned int>(f[k] >> 32) != ep) f[k] = ld_relaxed_u64(P.flags + t[k]);
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    double2 v[2][NORD];
+          for (int p = 0; p < NORD; ++p) ld_relaxed_v2(src + p, w[kk][p][0], w[kk][p][1]);
+        };
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const double2* src = (hi - (lane + 32 * k) == P.lb_D + 1) ? P.incl : P.agg;
+        for (int kk = 0; kk < KB; ++kk)
+          if (live[k0 + kk]) load(kk);
 #pragma unroll
-      for (int p = 0; p < NORD; ++p) v[k][p] = live[k] ? __ldcg(src + t[k] * NORD + p) : make_double2(0.0, 0.0);
-    }
+        for (int kk = 0; kk < KB; ++kk) {
+          if (!live[k0 + kk]) continue;
+          for (;;) {
+            bool ok = true;
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
-      if (lane + 32 * k < cnt) {
+            for (int p = 0; p < NORD; ++p) ok = ok && (w[kk][p][0] & 15ull) == tg && (w[kk][p][1] & 15ull) == tg;
+            if (ok) break;
+            load(kk);
+          }
+        }
 #pragma unroll
-        for (int p = 0; p < NORD; ++p) S.pay[lane + 32 * k][p] = v[k][p];
+        for (int kk = 0; kk < KB; ++kk) {
+          const int j = lane + 32 * (k0 + kk);
+          if (j < cnt) {
+#pragma unroll
+            for (int p = 0; p < NORD; ++p)
+              S.pay[j][p] = live[k0 + kk] ? make_double2(untag_word(w[kk][p][0]), untag_word(w[kk][p][1]))
+                                          : make_double2(0.0, 0.0);
+          }
+        }
       }
+    } else {
+      unsigned long long f[2] = {0ull, 0ull};
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if (live[k]) f[k] = ld_relaxed_u64(P.flags + t[k]);
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if (live[k])
+          while (static_cast<unsigned int>(f[k] >> 32) != ep) f[k] = ld_relaxed_u64(P.flags + t[k]);
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      double2 v[2][NORD];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double2* src = (hi - (lane + 32 * k) == P.lb_D + 1) ? P.incl : P.agg;
+#pragma unroll
+        for (int p = 0; p < NORD; ++p) v[k][p] = live[k] ? __ldcg(src + t[k] * NORD + p) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if (lane + 32 * k < cnt) {
+#pragma unroll
+          for (int p = 0; p < NORD; ++p) S.pay[lane + 32 * k][p] = v[k][p];
+        }
+    }
     __syncwarp();
     if (hi == P.lb_D + 1 && hi <= 64) {
       // Single round (the common case, D + 1 <= 64): G lane groups each Horner one
@@ -592,8 +650,15 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
       }
       S.tagg[p] = make_double2(static_cast<double>(X::re(a)), static_cast<double>(X::im(a)));
       S.tsfx[p] = make_double2(static_cast<double>(X::re(b2)), static_cast<double>(X::im(b2)));
+      if constexpr (sizeof(T) == 4) {
+        const unsigned long long tg = pay_tag(S.epoch);
+        st_relaxed_v2(P.agg + gt * NORD + p, tag_word(S.tagg[p].x, tg), tag_word(S.tagg[p].y, tg));
+        st_relaxed_v2(P.incl + gt * NORD + p, tag_word(S.tsfx[p].x, tg), tag_word(S.tsfx[p].y, tg));
+      }
     }
-    if (warp == 0) {
+    if constexpr (sizeof(T) == 4) {
+      trace_ev(P, gt, 3);
+    } else if (warp == 0) {
       __syncwarp();
       if (lane == 0) {
 #pragma unroll
