@@ -483,6 +483,36 @@ def test_plan_reuse_and_graph_capture(sft, O):
     assert torch.equal(o1, o2)
 
 
+@pytest.mark.parametrize("prec", [0, 1])
+def test_lookback_launch_tags_reject_stale_payloads(sft, O, prec):
+    """The look-back payloads of fp32 plans carry a launch tag (epoch mod 15) instead of
+    a flag, fp64 plans a flag with the full epoch: across 40 launches (the tag wraps
+    twice) over alternating inputs, every result equals that input's first result bit
+    for bit, so no tile ever consumed a predecessor's payload from an earlier launch."""
+    import torch
+
+    spec = sft.make_transform_spec("MDS5P6", 8192.0, 10.0, sft.TransformOptions(precision=prec))
+    n = 102400
+    pr = sft.Precision.Double if prec else sft.Precision.Single
+    xs = [sft.generate_signals(sft.TestSignalKind.SeededNoise, n, seed, 1, pr) for seed in (3, 4)]
+    plan = sft.TransformPlan(spec, n, mode="lookback")
+    assert plan.describe()["sequential"] == 0
+    refs = []
+    for x in xs:
+        o = plan.empty_output()
+        plan.execute(x, o)
+        refs.append(o)
+    o = plan.empty_output()
+    for i in range(40):
+        plan.execute(xs[i % 2], o)
+        torch.cuda.synchronize()
+        assert torch.equal(o, refs[i % 2]), i
+    xh = xs[1].double().cpu().numpy()[0]
+    got = refs[1].double().cpu().numpy()
+    got = got[..., 0] + 1j * got[..., 1]
+    assert rel_max(got[0], oracle_transform(O, xh, 1, spec)) < (1e-12 if prec else 1e-5)
+
+
 @pytest.mark.parametrize("mode", ["lookback", "seq"])
 def test_pipelined_host_execution(sft, O, mode):
     """sftgpu_transform_execute_host_async: a stream of distinct pinned host buffers, all
