@@ -548,9 +548,11 @@ struct Cx<float> {
   }
   static __device__ __forceinline__ S warp_sum(S v) {
 #pragma unroll
-    for (int d = 16; d >= 1; d >>= 1)
-      v = fma2(pk(1.0f, 1.0f), pk(__shfl_xor_sync(0xffffffffu, re(v), d), __shfl_xor_sync(0xffffffffu, im(v), d)), v);
+    for (int d = 16; d >= 1; d >>= 1) v = xor_add(v, d);
     return v;
+  }
+  static __device__ __forceinline__ S xor_add(S v, int d) {  // one butterfly level of warp_sum
+    return fma2(pk(1.0f, 1.0f), pk(__shfl_xor_sync(0xffffffffu, re(v), d), __shfl_xor_sync(0xffffffffu, im(v), d)), v);
   }
 };
 
@@ -586,6 +588,11 @@ struct Cx<double> {
     return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
   }
   static __device__ __forceinline__ S warp_sum(S v) { return warp_sum2(v); }
+  static __device__ __forceinline__ S xor_add(S v, int d) {  // one butterfly level of warp_sum
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, d);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, d);
+    return v;
+  }
 };
 
 // One tile: stage samples, phase 1, scans, carry (SEQ: from smem; LB: look-back),
@@ -618,24 +625,46 @@ __device__ __forceinline__ void do_tile(const ScanParams<T>& P, Smem<T, NORD, L,
 
   if constexpr (!SEQ) {
     // ---- lead-only aggregates (whole tile and its last r positions), published for
-    // the successors' window carries
-#pragma unroll
-    for (int p = 0; p < NORD; ++p) {
-      const OrdConst<T>& c = P.oc[p];
-      St la = X::zero(), sa = X::zero();
+    // the successors' window carries. Samples are read once, and every order's two sums
+    // go through the butterfly together (independent chains the scheduler interleaves;
+    // the tile's publication waits on this block).
+    {
+      T xv[L];
 #pragma unroll
       for (int i = 0; i < L; ++i) {
         const int e = tid * L + i;
-        const T xl = sl[e + (e >> 5)];
-        la = X::agg_r(c, i, xl, la);
-        sa = X::agg_r(c, i, e >= P.lb_sfx ? xl : T(0), sa);
+        xv[i] = sl[e + (e >> 5)];
       }
-      const T* rot = P.tab + (p * kTabStride + 31 - lane) * 4;  // z^{L(31-lane)} (prefetched)
-      la = X::warp_sum(X::madd(rot, la, X::zero()));
-      sa = X::warp_sum(X::madd(rot, sa, X::zero()));
+      St la[NORD], sa[NORD];
+#pragma unroll
+      for (int p = 0; p < NORD; ++p) {
+        const OrdConst<T>& c = P.oc[p];
+        la[p] = X::zero();
+        sa[p] = X::zero();
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+          const int e = tid * L + i;
+          la[p] = X::agg_r(c, i, xv[i], la[p]);
+          sa[p] = X::agg_r(c, i, e >= P.lb_sfx ? xv[i] : T(0), sa[p]);
+        }
+        const T* rot = P.tab + (p * kTabStride + 31 - lane) * 4;  // z^{L(31-lane)} (prefetched)
+        la[p] = X::madd(rot, la[p], X::zero());
+        sa[p] = X::madd(rot, sa[p], X::zero());
+      }
+#pragma unroll
+      for (int d = 16; d >= 1; d >>= 1) {
+#pragma unroll
+        for (int p = 0; p < NORD; ++p) {
+          la[p] = X::xor_add(la[p], d);
+          sa[p] = X::xor_add(sa[p], d);
+        }
+      }
       if (lane == 0) {
-        S.wla[warp][p] = make2<T2>(X::re(la), X::im(la));
-        S.wsa[warp][p] = make2<T2>(X::re(sa), X::im(sa));
+#pragma unroll
+        for (int p = 0; p < NORD; ++p) {
+          S.wla[warp][p] = make2<T2>(X::re(la[p]), X::im(la[p]));
+          S.wsa[warp][p] = make2<T2>(X::re(sa[p]), X::im(sa[p]));
+        }
       }
     }
     trace_ev(P, gt, 6);
