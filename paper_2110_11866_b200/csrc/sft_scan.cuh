@@ -252,7 +252,7 @@ struct Smem {
   // window carry (warp 0, after that barrier) reuses it.
   union {
     T2 wscan[NW][NORD * 33];          // per-warp transposed scan staging (padded)
-    double2 pay[SEQ ? 1 : 64][NORD];  // LB window-carry staging (64 predecessors per round)
+    double2 pay[SEQ ? 1 : (sizeof(T) == 8 ? 128 : 64)][NORD];  // LB window-carry staging (one round)
   };
   T2 wst[NW][NORD][4];              // per-warp segment starts of the transposed scan
   // powers for folding segment starts into thread states ({re, re, -im, im} entries):
@@ -287,23 +287,25 @@ __device__ __forceinline__ void trace_ev(const ScanParams<T>& P, long long gt, i
 // predecessors' lead-only aggregates (LA: whole tile, SA: its last r positions).
 // Every tile publishes (LA, SA) as soon as its samples are staged; nothing waits on a
 // chain of inclusive prefixes. Flags: (epoch << 32) | 1, payload LA in `agg`, SA in
-// `incl`. Staged 64 predecessors per round, Horner from the oldest (fp64).
+// `incl`. Staged 32 KS predecessors per round (KS per lane: 2 fp32, 4 fp64), Horner from
+// the oldest (fp64).
 template <typename T, int NORD, int L, int NT, bool SEQ>
 __device__ __forceinline__ void window_carry(const ScanParams<T>& P, Smem<T, NORD, L, NT, SEQ>& S, long long gt,
                                              long long first, int lane) {
   double2 acc = make_double2(0.0, 0.0);
   const double2 zT = lane < NORD ? P.tab_tile[lane * kTabTileStride] : make_double2(1.0, 0.0);
-  for (int hi = P.lb_D + 1; hi >= 1; hi -= 64) {
-    const int lo_d = hi - 63 > 1 ? hi - 63 : 1;
+  constexpr int KS = sizeof(T) == 8 ? 4 : 2, R = 32 * KS;  // predecessors per lane / round
+  for (int hi = P.lb_D + 1; hi >= 1; hi -= R) {
+    const int lo_d = hi - (R - 1) > 1 ? hi - (R - 1) : 1;
     const int cnt = hi - lo_d + 1;
-    // Each lane stages predecessors j = lane and lane + 32 in two round trips: both
-    // flags polled together (relaxed), one acquire fence, then both payloads in flight
-    // together (a poll + payload pair per predecessor would be four).
+    // Each lane stages predecessors j = lane + 32 k (k < KS) in two round trips: all its
+    // flags polled together (relaxed), one acquire fence, then all payloads in flight
+    // together (a poll + payload pair per predecessor would be 2 KS).
     const unsigned int ep = S.epoch;
-    long long t[2];
-    bool live[2];
+    long long t[KS];
+    bool live[KS];
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < KS; ++k) {
       const int j = lane + 32 * k;
       t[k] = gt - (hi - j);
       live[k] = j < cnt && t[k] >= first;
@@ -313,7 +315,7 @@ __device__ __forceinline__ void window_carry(const ScanParams<T>& P, Smem<T, NOR
       const unsigned long long tg = pay_tag(ep);
       constexpr int KB = NORD <= 8 ? 2 : 1;  // predecessors in flight per lane (registers)
 #pragma unroll
-      for (int k0 = 0; k0 < 2; k0 += KB) {
+      for (int k0 = 0; k0 < KS; k0 += KB) {
         unsigned long long w[KB][NORD][2];
         auto load = [&](int kk) {
           const int k = k0 + kk;
@@ -347,32 +349,31 @@ __device__ __forceinline__ void window_carry(const ScanParams<T>& P, Smem<T, NOR
         }
       }
     } else {
-      unsigned long long f[2] = {0ull, 0ull};
+      unsigned long long f[KS];
 #pragma unroll
-      for (int k = 0; k < 2; ++k)
-        if (live[k]) f[k] = ld_relaxed_u64(P.flags + t[k]);
+      for (int k = 0; k < KS; ++k) f[k] = live[k] ? ld_relaxed_u64(P.flags + t[k]) : 0ull;
 #pragma unroll
-      for (int k = 0; k < 2; ++k)
+      for (int k = 0; k < KS; ++k)
         if (live[k])
           while (static_cast<unsigned int>(f[k] >> 32) != ep) f[k] = ld_relaxed_u64(P.flags + t[k]);
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      double2 v[2][NORD];
+      double2 v[KS][NORD];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < KS; ++k) {
         const double2* src = (hi - (lane + 32 * k) == P.lb_D + 1) ? P.incl : P.agg;
 #pragma unroll
         for (int p = 0; p < NORD; ++p) v[k][p] = live[k] ? __ldcg(src + t[k] * NORD + p) : make_double2(0.0, 0.0);
       }
 #pragma unroll
-      for (int k = 0; k < 2; ++k)
+      for (int k = 0; k < KS; ++k)
         if (lane + 32 * k < cnt) {
 #pragma unroll
           for (int p = 0; p < NORD; ++p) S.pay[lane + 32 * k][p] = v[k][p];
         }
     }
     __syncwarp();
-    if (hi == P.lb_D + 1 && hi <= 64) {
-      // Single round (the common case, D + 1 <= 64): G lane groups each Horner one
+    if (hi == P.lb_D + 1 && hi <= R) {
+      // Single round (the common case, D + 1 <= R): G lane groups each Horner one
       // segment of the predecessors and scale it by z^{TT (cnt - segment end)} (host
       // table), then the groups are summed with shuffles: the fp64 dependency chain is
       // cnt / G long instead of cnt.
