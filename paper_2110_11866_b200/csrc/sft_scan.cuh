@@ -112,9 +112,10 @@ struct ScanParams {
   long long n_chunks;     // SEQ: chunks per signal
   int lb_D;               // LB: full tiles in the 2K window (2K = lb_D*TT + r)
   int lb_sfx;             // LB: first position of a tile's r-position suffix (TT if r == 0)
-  // ctrl[0] ticket, ctrl[1] finished-CTA count, ctrl[2] launch epoch. The last CTA
-  // of a launch resets ticket/count and bumps the epoch, so launches need no host
-  // state (graph-capturable) and stale look-back flags are ignored.
+  // ctrl[0..1]: 64-bit count of LB CTAs ever started on this plan. Every launch adds
+  // exactly total_tiles, so count / total_tiles numbers the launch (its epoch) without
+  // host state (graph-capturable) or a re-arming CTA; stale look-back payloads carry an
+  // older epoch.
   unsigned int* ctrl;
   unsigned long long* flags;
   double2* agg;
@@ -947,18 +948,13 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? (L >= 16 ? 5 : (N
   extern __shared__ __align__(16) unsigned char smem_raw[];  // sized by the launcher
   Smem<T, NORD, L, NT, SEQ>& S = *reinterpret_cast<Smem<T, NORD, L, NT, SEQ>*>(smem_raw);
   const int tid = threadIdx.x;
-  // LB: the ticket's round trip overlaps the table staging below (consumed after it)
-  // and the epoch read. The epoch only changes when this launch's last CTA re-arms the
-  // control block, after every CTA has counted in (after its ticket), so it can be read
-  // alongside the ticket.
-  unsigned int ticket = 0, epoch = 0;
+  // LB: count this CTA in; the result (the launch's epoch) is first needed when the
+  // tile publishes, so the round trip overlaps the table and sample staging
+  unsigned long long started = 0;
   unsigned long long t_entry = 0;
   if constexpr (!SEQ) {
     if constexpr (SFTK_TRACE) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
-    if (tid == 0) {
-      epoch = *reinterpret_cast<volatile unsigned int*>(P.ctrl + 2);
-      ticket = atomicAdd(P.ctrl, 1u);
-    }
+    if (tid == 0) started = atomicAdd(reinterpret_cast<unsigned long long*>(P.ctrl), 1ull);
   }
   if constexpr (!SEQ) {
     // tables read later on the tile's chain (lead-only warp sums, window carry): start
@@ -1011,17 +1007,9 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? (L >= 16 ? 5 : (N
       do_tile<T, NORD, NA, GM, MODE, L, NT, true>(P, S, sig, 0, 0, lo, count, obase, o_first + t * TT, xs,
                                                   t + 1 < tiles);
   } else {
-    if (tid == 0) {
-      S.tile = static_cast<long long>(ticket);
-      S.epoch = epoch;
-    }
-    __syncthreads();
-    // count in (after the ticket); inspected once this tile's loads are in flight. Every
-    // CTA has its ticket once the count is complete: the last one re-arms the control
-    // block (the next launch is stream-ordered after this one).
-    unsigned int counted = 0;
-    if (tid == 0) counted = atomicAdd(P.ctrl + 1, 1u);
-    const long long gt = S.tile;
+    // tiles in block order (dispatched in order, as in CUB's single-pass scan): a tile
+    // only waits on tiles of lower index, so staging starts at once
+    const long long gt = blockIdx.x;
     if constexpr (SFTK_TRACE) {
       if (P.trace && tid == 0) P.trace[gt * 8] = static_cast<long long>(t_entry);
     }
@@ -1031,11 +1019,8 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? (L >= 16 ? 5 : (N
     const long long o0 = (gt - first - P.warm_tiles) * TT;
     const T* __restrict__ xs = P.x + sig * P.ld_x;
     stage_tile<T, L, NT, false>(P, xs, P.lo, o0, tid, S.lead[0], S.trail[0]);
-    if (tid == 0 && counted == static_cast<unsigned int>(P.total_tiles - 1)) {
-      atomicExch(P.ctrl, 0u);
-      atomicExch(P.ctrl + 1, 0u);
-      atomicAdd(P.ctrl + 2, 1u);
-    }
+    // epoch >= 1: zero-initialised workspace never matches (read after do_tile's barrier)
+    if (tid == 0) S.epoch = static_cast<unsigned int>(started / static_cast<unsigned long long>(P.total_tiles)) + 1u;
     do_tile<T, NORD, NA, GM, MODE, L, NT, false>(P, S, sig, gt, first, P.lo, P.count, 0, o0, xs, false);
     if (o0 + TT > 0) trace_ev(P, gt, 5);
   }
