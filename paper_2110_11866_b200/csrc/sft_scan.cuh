@@ -967,27 +967,28 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? (L >= 16 ? 5 : (N
       if (tid < NORD) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.tab_tile + tid * kTabTileStride));
     }
   }
-  {
-    // every load issued before the first store (one round trip, not one per element)
-    using Sm = Smem<T, NORD, L, NT, SEQ>;
-    constexpr int E = Sm::SEG + Sm::SEGS;
-    constexpr int NQ = (NORD * E * 4 + NT - 1) / NT;
-    T v[NQ];
+  // segment-power table: every load issued now, stored after the tile's sample loads
+  // are in flight too (LB), so the two round trips overlap
+  using Sm = Smem<T, NORD, L, NT, SEQ>;
+  constexpr int E = Sm::SEG + Sm::SEGS;
+  constexpr int NQ = (NORD * E * 4 + NT - 1) / NT;
+  T ptv[NQ];
 #pragma unroll
-    for (int k = 0; k < NQ; ++k) {
-      const int q = tid + k * NT;
-      if (q < NORD * E * 4) {
-        const int p = q / (E * 4), j = (q / 4) % E, w = q % 4;
-        const int src = j < Sm::SEG ? j : Sm::SEG * (j - Sm::SEG);
-        v[k] = P.tab[(p * kTabStride + src) * 4 + w];
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < NQ; ++k) {
-      const int q = tid + k * NT;
-      if (q < NORD * E * 4) (&S.ptab[0][0][0])[q] = v[k];
+  for (int k = 0; k < NQ; ++k) {
+    const int q = tid + k * NT;
+    if (q < NORD * E * 4) {
+      const int p = q / (E * 4), j = (q / 4) % E, w = q % 4;
+      const int src = j < Sm::SEG ? j : Sm::SEG * (j - Sm::SEG);
+      ptv[k] = P.tab[(p * kTabStride + src) * 4 + w];
     }
   }
+  auto store_ptab = [&]() {
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      const int q = tid + k * NT;
+      if (q < NORD * E * 4) (&S.ptab[0][0][0])[q] = ptv[k];
+    }
+  };
 
   if constexpr (SEQ) {
     // one CTA per (signal, chunk): tiles in order from the chunk's own warm start,
@@ -1003,6 +1004,7 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? (L >= 16 ? 5 : (N
     const long long o_first = -P.warm_tiles * TT;
     const int b0 = static_cast<int>(((o_first / TT) % 2 + 2) % 2);
     stage_tile<T, L, NT, true>(P, xs, lo, o_first, tid, S.lead[b0], S.trail[b0]);
+    store_ptab();  // read after do_tile's first barrier
     for (long long t = 0; t < tiles; ++t)
       do_tile<T, NORD, NA, GM, MODE, L, NT, true>(P, S, sig, 0, 0, lo, count, obase, o_first + t * TT, xs,
                                                   t + 1 < tiles);
@@ -1019,6 +1021,7 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? (L >= 16 ? 5 : (N
     const long long o0 = (gt - first - P.warm_tiles) * TT;
     const T* __restrict__ xs = P.x + sig * P.ld_x;
     stage_tile<T, L, NT, false>(P, xs, P.lo, o0, tid, S.lead[0], S.trail[0]);
+    store_ptab();  // read after do_tile's first barrier
     // epoch >= 1: zero-initialised workspace never matches (read after do_tile's barrier)
     if (tid == 0) S.epoch = static_cast<unsigned int>(started / static_cast<unsigned long long>(P.total_tiles)) + 1u;
     do_tile<T, NORD, NA, GM, MODE, L, NT, false>(P, S, sig, gt, first, P.lo, P.count, 0, o0, xs, false);
