@@ -2,6 +2,7 @@
 // the kernel variants compile in parallel; sftgpu_api.cu only sees the declarations.
 #pragma once
 
+#include "device_util.cuh"
 #include "sft_scan.cuh"
 
 namespace sftk {
@@ -40,11 +41,9 @@ static void launch_fixed(const ScanParams<T>& p, long long grid, cudaStream_t s)
   constexpr size_t smem = sizeof(Smem<T, NORD, L, kThreads, SEQ>);
   auto* kern = &sft_scan_kernel<T, NORD, NA, KGM, MODE, L, kThreads, SEQ>;
   if constexpr (smem > 48 * 1024) {
-    // one process drives one GPU: the opt-in is made once per process
-    // (if it failed, the launch below fails and run_groups reports it)
-    static const cudaError_t opt_in =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    (void)opt_in;
+    // once per device (if it failed, the launch below fails and run_groups reports it)
+    static std::atomic<unsigned long long> opted{0};
+    (void)smem_opt_in(kern, static_cast<int>(smem), opted);
   }
   kern<<<grid, kThreads, smem, s>>>(p);
 }

@@ -1009,8 +1009,11 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? (L >= 16 ? 5 : (N
       do_tile<T, NORD, NA, GM, MODE, L, NT, true>(P, S, sig, 0, 0, lo, count, obase, o_first + t * TT, xs,
                                                   t + 1 < tiles);
   } else {
-    // tiles in block order (dispatched in order, as in CUB's single-pass scan): a tile
-    // only waits on tiles of lower index, so staging starts at once
+    // tiles in block order: a tile only waits on tiles of lower index, so staging starts
+    // at once. Forward progress assumes the hardware starts a grid's CTAs in blockIdx
+    // order (as CUB's single-pass scan does): a spinning CTA's predecessors have then all
+    // started and never wait on it. This holds with other kernels running concurrently
+    // (the scalogram's streams): they only delay when this grid's next CTA starts.
     const long long gt = blockIdx.x;
     if constexpr (SFTK_TRACE) {
       if (P.trace && tid == 0) P.trace[gt * 8] = static_cast<long long>(t_entry);
@@ -1022,7 +1025,8 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? (SEQ ? (L >= 16 ? 5 : (N
     const T* __restrict__ xs = P.x + sig * P.ld_x;
     stage_tile<T, L, NT, false>(P, xs, P.lo, o0, tid, S.lead[0], S.trail[0]);
     store_ptab();  // read after do_tile's first barrier
-    // epoch >= 1: zero-initialised workspace never matches (read after do_tile's barrier)
+    // epoch >= 1 (read after do_tile's barrier). The plan zeroes its flags and payloads:
+    // flag epoch 0 and payload tag 0 never match a live launch.
     if (tid == 0) S.epoch = static_cast<unsigned int>(started / static_cast<unsigned long long>(P.total_tiles)) + 1u;
     do_tile<T, NORD, NA, GM, MODE, L, NT, false>(P, S, sig, gt, first, P.lo, P.count, 0, o0, xs, false);
     if (o0 + TT > 0) trace_ev(P, gt, 5);

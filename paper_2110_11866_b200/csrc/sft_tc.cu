@@ -1,5 +1,6 @@
 // K4 launch (tensor-core chunked transform). The kernel lives in sft_tc.cuh; the
 // operand image and the per-order constants are built by the plan (sftgpu_api.cu).
+#include "device_util.cuh"
 #include "sft_tc.cuh"
 #include "sft_tc_launch.h"
 
@@ -7,8 +8,8 @@ namespace tck {
 
 template <int NORD>
 static cudaError_t launch_n(const TcParams& p, int grid, cudaStream_t s) {
-  static const cudaError_t opt_in = cudaFuncSetAttribute(
-      sft_tc_kernel<NORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+  static std::atomic<unsigned long long> opted{0};  // once per device
+  const cudaError_t opt_in = sftk::smem_opt_in(sft_tc_kernel<NORD>, static_cast<int>(kSmemBytes), opted);
   if (opt_in != cudaSuccess) return opt_in;
   sft_tc_kernel<NORD><<<grid, kThreads, kSmemBytes, s>>>(p);
   return cudaGetLastError();

@@ -114,7 +114,13 @@ struct sftgpu_plan {
   long long TT = 1024, tiles_per_signal = 0, warm_tiles = 0, total_tiles = 0;
   std::vector<Group> groups;
   int max_nord = 1;
-  unsigned int* d_ctrl = nullptr;  // ticket, done count, epoch (device-managed)
+  unsigned int* d_ctrl = nullptr;  // LB: 64-bit count of CTAs ever started (launch epochs)
+  // LB launches of one plan share the workspace and number themselves from d_ctrl, so
+  // they must never overlap: each launch waits on the event the previous one recorded
+  // when it was issued on a different stream (same stream: already ordered)
+  cudaEvent_t ev_lb = nullptr;
+  cudaStream_t lb_stream = nullptr;
+  bool lb_recorded = false;
   unsigned long long* d_flags = nullptr;
   double2* d_agg = nullptr;
   double2* d_incl = nullptr;
@@ -177,6 +183,7 @@ struct sftgpu_plan {
       cudaFree(sb_out[k]);
     }
     cudaFree(d_tc_image);
+    if (ev_lb) cudaEventDestroy(ev_lb);
     cudaFree(d_ctrl);
     cudaFree(d_flags);
     cudaFree(d_agg);
@@ -413,7 +420,7 @@ void build_groups(sftgpu_plan* pl, std::vector<Order> ords, double alpha, double
 // with look-back. Auto picks SEQ when the (signal, chunk) grid gives >= 2 CTAs per SM.
 void choose_geometry(sftgpu_plan* pl) {
   const bool dbl = pl->precision == SFTGPU_DOUBLE;
-  constexpr long long kSms = 148, kTarget = 4 * kSms;
+  const long long kSms = sftk::sm_count(), kTarget = 4 * kSms;
   pl->NT = sftk::kThreads;
   const long long tt_seq = static_cast<long long>(dbl ? sftk::kLSeqF64 : sftk::kLSeqF32) * pl->NT;
   const long long cmin = ((std::max(8 * tt_seq, 16LL * pl->K) + tt_seq - 1) / tt_seq) * tt_seq;
@@ -450,14 +457,39 @@ void choose_geometry(sftgpu_plan* pl) {
 void alloc_workspace(sftgpu_plan* pl) {
   if (pl->seq) return;  // SEQ mode needs no inter-CTA state
   if (pl->total_tiles >= (1LL << 31)) fail(SFTGPU_EINVAL, "problem too large for one plan (tiles >= 2^31)");
-  const unsigned int ctrl0[4] = {0u, 0u, 1u, 0u};  // epoch starts at 1: zeroed flags are stale
-  cuda_check(cudaMalloc(&pl->d_ctrl, sizeof(ctrl0)), "cudaMalloc ctrl");
-  cuda_check(cudaMemcpy(pl->d_ctrl, ctrl0, sizeof(ctrl0), cudaMemcpyHostToDevice), "init ctrl");
+  // ctrl[0..1]: the 64-bit started-CTA count (launch k has epoch k + 1 >= 1)
+  cuda_check(cudaMalloc(&pl->d_ctrl, 4 * sizeof(unsigned int)), "cudaMalloc ctrl");
+  cuda_check(cudaMemset(pl->d_ctrl, 0, 4 * sizeof(unsigned int)), "init ctrl");
   cuda_check(cudaMalloc(&pl->d_flags, pl->total_tiles * sizeof(unsigned long long)), "cudaMalloc flags");
   cuda_check(cudaMemset(pl->d_flags, 0, pl->total_tiles * sizeof(unsigned long long)), "memset flags");
+  // Payloads are zeroed too: fp32 plans accept a payload word by its launch tag (low 4
+  // bits, 1..15) and a zero word carries tag 0, which never matches. Without this a new
+  // plan could accept the tagged payloads a freed plan left at the same address.
   const size_t pay = static_cast<size_t>(pl->total_tiles) * pl->max_nord * sizeof(double2);
   cuda_check(cudaMalloc(&pl->d_agg, pay), "cudaMalloc aggregates");
   cuda_check(cudaMalloc(&pl->d_incl, pay), "cudaMalloc prefixes");
+  cuda_check(cudaMemset(pl->d_agg, 0, pay), "memset aggregates");
+  cuda_check(cudaMemset(pl->d_incl, 0, pay), "memset prefixes");
+  cuda_check(cudaEventCreateWithFlags(&pl->ev_lb, cudaEventDisableTiming), "event create");
+  cuda_check(cudaStreamSynchronize(nullptr), "workspace init");  // memsets done before any launch
+}
+
+// Orders an LB launch after the plan's previous one (see sftgpu_plan::ev_lb). During
+// stream capture the graph's own edges order the launches (one capture chain per plan).
+bool lb_capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cuda_check(cudaStreamIsCapturing(st, &cs), "cudaStreamIsCapturing");
+  return cs != cudaStreamCaptureStatusNone;
+}
+void lb_order_begin(sftgpu_plan* pl, cudaStream_t st, bool capturing) {
+  if (capturing || !pl->lb_recorded || pl->lb_stream == st) return;
+  cuda_check(cudaStreamWaitEvent(st, pl->ev_lb, 0), "stream wait (look-back ordering)");
+}
+void lb_order_end(sftgpu_plan* pl, cudaStream_t st, bool capturing) {
+  if (capturing) return;
+  cuda_check(cudaEventRecord(pl->ev_lb, st), "event record (look-back ordering)");
+  pl->lb_stream = st;
+  pl->lb_recorded = true;
 }
 
 
@@ -497,7 +529,7 @@ bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
     const char* env = std::getenv("SFTGPU_NO_TC");
     if (env && env[0] == '1') return false;
     const long long tiles = pl->batch * ((pl->count + tck::kTile - 1) / tck::kTile);
-    if (tiles < 4LL * 148) return false;
+    if (tiles < 4LL * sftk::sm_count()) return false;
   }
   const bool cplx = lw.complex_out;
   const int nord = static_cast<int>(ords.size());
@@ -594,7 +626,7 @@ bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
   cuda_check(cudaMalloc(&pl->d_tc_image, img.size()), "cudaMalloc tc image");
   cuda_check(cudaMemcpy(pl->d_tc_image, img.data(), img.size(), cudaMemcpyHostToDevice), "copy tc image");
   // geometry: items = (signal, chunk); one persistent CTA per SM walks items in order
-  constexpr long long kSms = 148;
+  const long long kSms = sftk::sm_count();
   const long long tiles_sig = (pl->count + tck::kTile - 1) / tck::kTile;
   long long chunks = 1;
   if (pl->batch < kSms) chunks = std::min(tiles_sig, (kSms + pl->batch - 1) / pl->batch);
@@ -958,6 +990,9 @@ void run_groups(sftgpu_plan* pl, const void* x, long long ld_x, void* out, void*
     if constexpr (std::is_same<T, float>::value) run_tc(pl, x, ld_x, out, ld_out, st);
     return;
   }
+  const bool lb = !pl->seq && pl->d_ctrl != nullptr;
+  const bool capturing = lb && lb_capturing(st);
+  if (lb) lb_order_begin(pl, st, capturing);
   for (size_t gi = 0; gi < pl->groups.size(); ++gi) {
     Group& g = pl->groups[gi];
     sftk::ScanParams<T> P = params_of<T>(g);
@@ -1002,6 +1037,7 @@ void run_groups(sftgpu_plan* pl, const void* x, long long ld_x, void* out, void*
     launch_scan<T>(pl, g, P, st);
     cuda_check(cudaGetLastError(), "sft_scan_kernel launch");
   }
+  if (lb) lb_order_end(pl, st, capturing);
 }
 
 // GCT3/MCT3 (proj/src/transforms.cpp:430-442): fp64 accumulation into a complex
@@ -1547,7 +1583,7 @@ int sftgpu_generate_signal(int kind, int64_t n, uint64_t seed, int64_t batch, in
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const long long total = n * batch;
     const int threads = 256;
-    const long long blocks = std::min<long long>((total + threads - 1) / threads, 148LL * 16);
+    const long long blocks = std::min<long long>((total + threads - 1) / threads, sftk::sm_count() * 16LL);
     if (dtype == SFTGPU_SINGLE)
       sftk::generate_signal_kernel<float><<<blocks, threads, 0, st>>>(kind, n, seed, batch, static_cast<float*>(out));
     else

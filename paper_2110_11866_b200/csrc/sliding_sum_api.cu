@@ -1,4 +1,4 @@
-// C ABI for the GPU sliding sums (K4 flat, K5 blocked8) plus the reference's plan /
+// C ABI for the GPU sliding sums (K5 flat, K6 blocked8) plus the reference's plan /
 // cost-model arithmetic (proj/include/sft/sliding_sum.hpp:23-64, proj/src/sliding_sum.cpp:7-40).
 #include <cuda_runtime.h>
 
@@ -6,6 +6,7 @@
 #include <string>
 
 #include "../../include/sftgpu.h"
+#include "device_util.cuh"
 #include "sliding_sum.cuh"
 
 extern "C" const char* sftgpu_last_error(void);
@@ -87,7 +88,7 @@ int run(int blocked, const void* f, const SsPlan& p, void* out, cudaStream_t st)
   const int threads = 256;
   const long long count = p.n - p.L + 1;
   if (!blocked) {
-    const long long blocks = std::min<long long>((p.n + threads - 1) / threads, 148LL * 32);
+    const long long blocks = std::min<long long>((p.n + threads - 1) / threads, sftk::sm_count() * 32LL);
     for (int r = 0; r < p.rounds; ++r) {
       sftk::sliding_flat_round<T><<<blocks, threads, 0, st>>>(g1, h1, g2, h2, p.n, 1LL << r,
                                                               static_cast<int>((p.L >> r) & 1));
@@ -108,7 +109,7 @@ int run(int blocked, const void* f, const SsPlan& p, void* out, cudaStream_t st)
       rest /= 8;
       ++stage;
     }
-    const long long blocks = std::min<long long>((count + threads - 1) / threads, 148LL * 32);
+    const long long blocks = std::min<long long>((count + threads - 1) / threads, sftk::sm_count() * 32LL);
     sftk::sliding_blocked8_gather<T><<<blocks, threads, 0, st>>>(h1, static_cast<T*>(out), count, stage, cols);
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return fail(e);

@@ -190,9 +190,14 @@ class ComponentsPlan:
         self._destroy = lib().sftgpu_plan_destroy
         self.n_orders, self.n, self.batch, self.count = len(cfgs), n, batch, hi - lo + 1
         self.precision = Precision(cfgs[0].precision)
+        self.device = _torch().cuda.current_device()
 
     def execute(self, x, c, s, stream=None):
         torch = _torch()
+        dt = torch.float32 if self.precision == Precision.Single else torch.float64
+        _check_device_buffer(x, dt, self.batch * self.n, self.device, "x")
+        for name, t in (("c", c), ("s", s)):
+            _check_device_buffer(t, dt, self.n_orders * self.batch * self.count, self.device, name)
         st = C.c_void_p(stream) if stream is not None else _stream_ptr(torch)
         check(lib().sftgpu_components_execute(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(c.data_ptr()), C.c_void_p(s.data_ptr()), st))
 
@@ -572,6 +577,39 @@ def _host_ptr(a) -> int:
     return a.__array_interface__["data"][0]
 
 
+def _check_device_buffer(t, dtype, need: int, device: int, name: str) -> None:
+    """Plans take raw device pointers: a wrong dtype, a strided view, another device or a
+    short buffer would be read or written out of bounds by the kernels. ``need`` is the
+    minimum element count."""
+    if not hasattr(t, "data_ptr") or not getattr(t, "is_cuda", False):
+        raise ValueError(f"{name}: expected a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name}: dtype {t.dtype} does not match the plan ({dtype})")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: tensor must be contiguous")
+    if t.device.index != device:
+        raise ValueError(f"{name}: tensor is on cuda:{t.device.index}, the plan on cuda:{device}")
+    if t.numel() < need:
+        raise ValueError(f"{name}: {t.numel()} elements, the plan needs {need}")
+
+
+def _check_host_buffer(a, itemsize: int, need: int, name: str) -> None:
+    """Host buffers of the *_host entry points: numpy arrays or CPU tensors, C-contiguous,
+    of the plan's element size and at least ``need`` elements."""
+    if hasattr(a, "data_ptr"):
+        if getattr(a, "is_cuda", False):
+            raise ValueError(f"{name}: expected a host buffer, got a CUDA tensor")
+        ok, size, n = a.is_contiguous(), a.element_size(), a.numel()
+    else:
+        ok, size, n = a.flags.c_contiguous, a.itemsize, a.size
+    if not ok:
+        raise ValueError(f"{name}: host buffer must be C-contiguous")
+    if size != itemsize:
+        raise ValueError(f"{name}: element size {size} does not match the plan ({itemsize})")
+    if n < need:
+        raise ValueError(f"{name}: {n} elements, the plan needs {need}")
+
+
 class TransformPlan:
     """Device plan: ``batch`` signals of ``n`` samples -> transform output, all in HBM.
     x: [batch][ld_x] (float32 for Single, float64 for Double); out: [batch][ld_out]
@@ -593,6 +631,8 @@ class TransformPlan:
         conv = spec.kind in (TransformKind.TruncConvGauss, TransformKind.TruncConvMorlet)
         self.precision = Precision.Double if conv else spec.precision
         self.launches = lib().sftgpu_plan_launches_per_execute(h)
+        self.device = _torch().cuda.current_device()
+        self._cw = 2 if self.complex_out else 1
 
     def describe(self) -> dict:
         info = (C.c_int64 * 11)()
@@ -616,13 +656,26 @@ class TransformPlan:
         return torch.empty(shape, dtype=self.dtype(), device="cuda")
 
     def execute(self, x, out, stream=None, ld_x=None, ld_out=None):
+        """x: [batch][ld_x] and out: [batch][ld_out](x2 complex) contiguous CUDA tensors of
+        the plan's dtype on the plan's device. One plan runs on one stream at a time;
+        launches on a new stream are ordered after the plan's previous launch."""
         torch = _torch()
+        lx, lo = ld_x or self.n, ld_out or self.count
+        dt = self.dtype()
+        _check_device_buffer(x, dt, (self.batch - 1) * lx + self.n, self.device, "x")
+        _check_device_buffer(out, dt, ((self.batch - 1) * lo + self.count) * self._cw, self.device, "out")
         st = C.c_void_p(stream) if stream is not None else _stream_ptr(torch)
-        check(lib().sftgpu_transform_execute(self._h, C.c_void_p(x.data_ptr()), ld_x or self.n,
-                                             C.c_void_p(out.data_ptr()), ld_out or self.count, st))
+        check(lib().sftgpu_transform_execute(self._h, C.c_void_p(x.data_ptr()), lx,
+                                             C.c_void_p(out.data_ptr()), lo, st))
+
+    def _check_host(self, x_host, out_host):
+        isz = 4 if self.precision == Precision.Single else 8
+        _check_host_buffer(x_host, isz, self.batch * self.n, "x_host")
+        _check_host_buffer(out_host, isz, self.batch * self.count * self._cw, "out_host")
 
     def execute_host(self, x_host: np.ndarray, out_host: np.ndarray, stream=None):
         torch = _torch()
+        self._check_host(x_host, out_host)
         st = C.c_void_p(stream) if stream is not None else _stream_ptr(torch)
         check(lib().sftgpu_transform_execute_host(self._h, C.c_void_p(_host_ptr(x_host)),
                                                   C.c_void_p(_host_ptr(out_host)), st))
@@ -630,6 +683,7 @@ class TransformPlan:
     def execute_host_async(self, x_host: np.ndarray, out_host: np.ndarray, stream=None):
         """Pipelined host-buffer execution (``sftgpu_transform_execute_host_async``): returns
         once queued; ``stream`` (default: torch's current) waits for the result copy."""
+        self._check_host(x_host, out_host)
         st = C.c_void_p(stream) if stream is not None else _stream_ptr(_torch())
         check(lib().sftgpu_transform_execute_host_async(self._h, C.c_void_p(_host_ptr(x_host)),
                                                         C.c_void_p(_host_ptr(out_host)), st))
