@@ -7,8 +7,10 @@ one signal. ``--workload`` selects the other BASELINE configs (1, 2, 4, 5).
 
 Arms:
   --impl ours (default)   the product: libsftgpu (K4 tensor-core / K1 scan kernels) through the C ABI.
-  --impl reference        the reference's CPU path (restated in oracle/, the reference
-                          itself does not build here: no Eigen3) on all host threads.
+  --impl reference        the reference's CPU path on all host threads: the reference
+                          library compiled from its own sources (oracle/_ref, built by
+                          oracle/ref.mk with a mini-Eigen shim), Recursive2 fp64 (its
+                          bench default); the restated port in oracle/ if that build is absent.
 Multi-GPU: one process per GPU (torchrun); single-signal workloads run independent
 replicas ("replicas only"); the scalogram shards scales across ranks.
 """
@@ -28,6 +30,8 @@ sys.path.insert(0, ROOT)
 
 L2_BYTES = 126 * 1024 * 1024
 PAPER_MS = 0.545  # PAPER.md:28-30, RTX 3090, N=102400, sigma=8192
+METRIC = "Morlet transform ms @N=102400,σ=8192; Msamples·scales/s; HBM GB/s vs peak"
+UNIT = "Msamples·scales/s"
 
 WORKLOADS = {
     # BASELINE config 3 (headline)
@@ -181,70 +185,109 @@ def ncu_traffic(workload: str):
 
 
 # ------------------------------------------------------------------ reference arm (CPU)
-def oracle_run(O, spec, x, workers):
-    """The reference's CPU transform (restated, oracle/) for one signal, with the
-    reference's default strategy (Recursive2, proj/src/eval.cpp:186-189)."""
-    k = int(spec.kind)
-    prec = int(spec.precision)
-    gamma = 1.0 / (2.0 * spec.sigma ** 2)
-    if k <= 2:
-        b = spec.gauss_coeffs
-        return O.gauss_smooth(x, 1, k, spec.half_width, spec.beta, spec.n0, spec.alpha, gamma, O.RECURSIVE2, prec,
-                              b.a, b.b, b.d, workers)
-    if k == 3:
-        c = spec.morlet_coeffs
-        return O.morlet_direct(x, 1, spec.half_width, spec.beta, spec.n0, spec.alpha, gamma, O.RECURSIVE2, prec,
-                               c.cos_orders, c.cos_coeffs, c.sin_orders, c.sin_coeffs, workers)
-    e = spec.envelope_coeffs
-    return O.morlet_multiply(x, 1, spec.half_width, spec.beta, spec.n0, spec.alpha, spec.sigma, spec.xi,
-                             O.RECURSIVE2, prec, e.cos_coeffs.real, workers)
+def workload_config(args, w, abbrev, K):
+    """The config object both arms print (identical keys and values)."""
+    world = args.gpus
+    return {"workload": args.workload, "desc": w["desc"], "abbreviation": abbrev, "K": K, "batch": w["batch"],
+            "n": w["n"], "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
 
 
-def cpu_measure(spec, w, steps, warmup, sample_signals):
-    """Times the CPU reference path on `sample_signals` signals per step, all host threads."""
+def cpu_reference_measure(w, steps, warmup, sample_signals, strategy=None, precision=None):
+    """Times the reference's own CPU transform: the library compiled from
+    /root/reference/proj/src by oracle/ref.mk (oracle/_ref, kind "reference"); where that
+    build is absent, the restated port in oracle/ (kind "port"). Spec built by the
+    reference's own factory, untimed (as proj/src/eval.cpp:186-190); default engine =
+    the reference bench's Recursive2 (eval.cpp:187) in fp64. Median of ``steps`` after
+    ``warmup`` (eval.cpp:192-203), all host threads as workers. Returns a dict."""
+    cores = os.cpu_count() or 1
+    strategy = 2 if strategy is None else strategy
+    precision = 1 if precision is None else precision
+    try:
+        import oracle.ref as R
+
+        R.lib()
+        kind = "reference"
+    except Exception:  # noqa: BLE001  (no reference build on this box)
+        R, kind = None, "port"
     import oracle as O
 
-    cores = os.cpu_count() or 1
     xs = [O.make_test_signal(O.SEEDED_NOISE, w["n"], 1234 + i) for i in range(sample_signals)]
-    if w["precision"] == 0:
-        xs = [x.astype("float32").astype("float64") for x in xs]
+    if R is not None:
+        spec = R.Spec(w["abbrev"], w["sigma"], w["xi"], strategy=strategy, precision=precision)
+        K = spec.half_width
+        run = lambda x: R.apply_transform(spec, x, 1, cores)  # noqa: E731
+    else:
+        spec = _port_spec(w)
+        K = spec["K"]
+        run = lambda x: _port_run(O, spec, x, strategy, precision, cores)  # noqa: E731
     for _ in range(warmup):
-        oracle_run(O, spec, xs[0], cores)
+        run(xs[0])
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
         for x in xs:
-            oracle_run(O, spec, x, cores)
+            run(x)
         times.append(time.perf_counter() - t0)
     t = statistics.median(times)
-    return sample_signals * w["n"] / t / 1e6, t, cores
+    return {"value": sample_signals * w["n"] / t / 1e6, "seconds": t, "cores": cores, "kind": kind, "K": K,
+            "strategy": ["KernelIntegral", "Recursive1", "Recursive2"][strategy],
+            "precision": ["f32", "f64"][precision]}
 
 
-def run_reference(args, w, spec_of):
+def _port_spec(w):
+    """Restated-oracle fallback: the spec fixture written beside the oracle by
+    oracle/make_bench_specs.py (so this arm never loads the product library)."""
+    with open(os.path.join(ROOT, "oracle", "bench_specs.json")) as f:
+        return json.load(f)[w["abbrev"] + f"@{w['sigma']:g}"]
+
+
+def _port_run(O, spec, x, strategy, precision, workers):
+    import numpy as np
+
+    k = spec["kind"]
+    gamma = 1.0 / (2.0 * spec["sigma"] ** 2)
+    if k <= 2:
+        return O.gauss_smooth(x, 1, k, spec["K"], spec["beta"], spec["n0"], spec["alpha"], gamma, strategy, precision,
+                              np.array(spec["a"]), np.array(spec["b"]), np.array(spec["d"]), workers)
+    cc = np.array(spec["cos_coeffs"][0]) + 1j * np.array(spec["cos_coeffs"][1])
+    if k == 3:
+        sc = np.array(spec["sin_coeffs"][0]) + 1j * np.array(spec["sin_coeffs"][1])
+        return O.morlet_direct(x, 1, spec["K"], spec["beta"], spec["n0"], spec["alpha"], gamma, strategy, precision,
+                               spec["cos_orders"], cc, spec["sin_orders"], sc, workers)
+    return O.morlet_multiply(x, 1, spec["K"], spec["beta"], spec["n0"], spec["alpha"], spec["sigma"], spec["xi"],
+                             strategy, precision, cc.real, workers)
+
+
+def run_reference(args, w):
+    """--impl reference: the reference's CPU path on this box's host cores, rank 0 only
+    (other ranks exit without work), same metric / unit / config as our arm."""
     rank = env_int("RANK", 0)
     if rank != 0:
         return
-    spec = spec_of()
     sample = 1 if w["batch"] == 1 else 2
-    value, t, cores = cpu_measure(spec, w, args.steps, args.warmup, sample)
+    m = cpu_reference_measure(w, args.steps, max(2, args.warmup), sample)
+    f32 = cpu_reference_measure(w, max(5, min(args.steps, 7)), 2, sample, precision=0)
+    value = m["value"]
     line = {
         "impl": "reference",
-        "metric": "Morlet transform ms @N=102400,σ=8192; Msamples·scales/s; HBM GB/s vs peak",
-        "value": value, "unit": "Msamples·scales/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3 / sample, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": value / (w["n"] / (PAPER_MS * 1e-3) / 1e6) if w["n"] == 102400 else None,
-        "dtype": "f32" if w["precision"] == 0 else "f64", "data": "synthetic (splitmix64 noise, seed 1234+i)",
-        "config": {"workload": args.workload, "desc": w["desc"], "strategy": "Recursive2 (reference default)"},
-        "cpu_baseline": {"value": value, "unit": "Msamples·scales/s", "cores": cores, "kind": "port",
-                         "sample": f"{sample} signal(s) of N={w['n']} per step, median of {args.steps}"},
-        "e2e": {"value": value, "unit": "Msamples·scales/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": max(2, args.warmup), "ms_per_step": m["seconds"] * 1e3 / sample, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": m["precision"], "data": "synthetic (splitmix64 noise, seed 1234+i, make_test_signal)",
+        "config": workload_config(args, w, w["abbrev"], m["K"]),
+        "engine": f"{m['strategy']} {m['precision']} (the reference bench default, proj/src/eval.cpp:186-189)",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": m["cores"], "kind": m["kind"],
+                         "sample": f"{sample} signal(s) of N={w['n']} per step, median of {args.steps} steps after "
+                                   f"{max(2, args.warmup)} warm-ups, {m['strategy']} {m['precision']}, "
+                                   f"workers={m['cores']} (the reference parallelises over orders)"},
+        "f32_recursive2": {"value": f32["value"], "unit": UNIT, "ms_per_signal": f32["seconds"] * 1e3 / sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ our arm (GPU)
 def run_ours(args, w, spec_of):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -260,44 +303,56 @@ def run_ours(args, w, spec_of):
     in_es = 4 if w["precision"] == 0 else 8
     out_es = in_es * (2 if plan.complex_out else 1)
     step_bytes = batch * n * (in_es + out_es)
-    R = max(1, math.ceil(3 * L2_BYTES / step_bytes)) if step_bytes < 3 * L2_BYTES else 1
-    R = min(R, 512)
     prec = P.Precision.Single if w["precision"] == 0 else P.Precision.Double
-    xs = [P.generate_signals(P.TestSignalKind.SeededNoise, n, 1234 + rank * 7919, batch, prec) for _ in range(min(R, 2))]
-    xs = [xs[i % len(xs)] if i < 2 else xs[i % 2].clone() for i in range(R)]
-    outs = [plan.empty_output() for _ in range(R)]
+    # Inputs: two distinct signals (batches), alternated; L2 state between steps: steps
+    # whose working set fits in L2 are preceded by a write of 2x L2 (cold start for every
+    # timed transform), larger steps stream more than L2 by themselves.
+    cold_flush = step_bytes < L2_BYTES
+    xs = [P.generate_signals(P.TestSignalKind.SeededNoise, n, 1234 + rank * 7919 + 17 * i, batch, prec)
+          for i in range(2)]
+    outs = [plan.empty_output() for _ in range(2)]
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device="cuda") if cold_flush else None
     torch.cuda.synchronize()
 
     stream = torch.cuda.Stream()
+    K = args.steps
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
-            plan.execute(xs[i % R], outs[i % R])
+            plan.execute(xs[i % 2], outs[i % 2])
         stream.synchronize()
+        # per-step CUDA events around the transform only (the L2 flush between steps is
+        # outside them), captured in a graph with the steps (external event nodes)
+        evs = [(torch.cuda.Event(enable_timing=True, external=True),
+                torch.cuda.Event(enable_timing=True, external=True)) for _ in range(K)]
+
+        def steps_body():
+            for k in range(K):
+                if flush is not None:
+                    flush.fill_(k)
+                evs[k][0].record(stream)
+                plan.execute(xs[k % 2], outs[k % 2])
+                evs[k][1].record(stream)
+
         graph = None
         if not args.no_graph:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=stream):
-                for k in range(args.steps):
-                    plan.execute(xs[k % R], outs[k % R])
+                steps_body()
             graph.replay()  # one untimed replay (graph upload)
             stream.synchronize()
 
         def timed_region():
-            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
-            ev0.record(stream)
             if graph is not None:
                 graph.replay()
             else:
-                for k in range(args.steps):
-                    plan.execute(xs[k % R], outs[k % R])
-            ev1.record(stream)
+                steps_body()
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
-            return ev0.elapsed_time(ev1)
+            return sum(e0.elapsed_time(e1) for e0, e1 in evs)
 
         with ClockSampler(device_index(args, local)) as clk:
             ms = timed_region()
@@ -308,23 +363,23 @@ def run_ours(args, w, spec_of):
                 graph.replay()
                 stream.synchronize()
     ms = max_over_ranks(ms, world)
-    ms_per_step = ms / args.steps
-    samples = n * batch * args.steps * world
+    ms_per_step = ms / K
+    samples = n * batch * K * world
     value = samples / (ms * 1e-3) / 1e6
 
     # e2e through the C ABI with pinned host buffers: every step copies its input H2D and
     # its result D2H. Small steps use the pipelined entry point over a ring of distinct
-    # host buffer pairs (copies of step k±1 overlap the kernel of step k); steps too large
+    # host buffer pairs (copies of step k+-1 overlap the kernel of step k); steps too large
     # for a pinned ring run the synchronous call.
     host_step = batch * n * (in_es + out_es)
     pairs = 3 if 3 * host_step <= (2 << 30) else 1
     x_hosts, o_hosts = [], []
     for i in range(pairs):
         xh = torch.empty((batch, n), dtype=plan.dtype()).pin_memory()
-        xh.copy_(xs[i % len(xs)].cpu())
+        xh.copy_(xs[i % 2].cpu())
         x_hosts.append(xh)
         o_hosts.append(torch.empty(outs[0].shape, dtype=plan.dtype()).pin_memory())
-    e2e_steps = max(1, min(args.steps * 10, 300)) if pairs > 1 else max(1, min(args.steps, 3))
+    e2e_steps = max(1, min(K * 10, 300)) if pairs > 1 else max(1, min(K, 3))
 
     def e2e_run(steps):
         for i in range(steps):
@@ -344,7 +399,8 @@ def run_ours(args, w, spec_of):
     e2e_value = n * batch * e2e_steps * world / max_over_ranks(e2e_s, world) / 1e6
     e2e_path = ("sftgpu_transform_execute_host_async (C ABI, pipelined over 3 pinned host buffer pairs; "
                 "wall clock around all steps + final stream sync)" if pairs > 1 else
-                "sftgpu_transform_execute_host (C ABI, pinned host buffers, one synchronous call per step; large tensor-core plans pipeline sub-batches inside the call)")
+                "sftgpu_transform_execute_host (C ABI, pinned host buffers, one synchronous call per step; "
+                "large tensor-core plans pipeline sub-batches inside the call)")
 
     peak, peak_src = measured_peaks()
     launches = plan.launches
@@ -355,36 +411,36 @@ def run_ours(args, w, spec_of):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         sample = 1 if batch == 1 else 2
-        cval, ct, cores = cpu_measure(spec, w, 3, 1, sample)
-        cpu = {"value": cval, "unit": "Msamples·scales/s", "cores": cores, "kind": "port",
-               "sample": f"{sample} signal(s) of N={n} per step (reference CPU path restated in oracle/, "
-                         f"Recursive2, all {cores} host threads), median of 3 after 1 warm-up",
-               "ms_per_signal": ct * 1e3 / sample}
+        m = cpu_reference_measure(w, 5, 2, sample)
+        cpu = {"value": m["value"], "unit": UNIT, "cores": m["cores"], "kind": m["kind"],
+               "sample": f"{sample} signal(s) of N={n} per step ({'the reference compiled from its sources, oracle/_ref' if m['kind'] == 'reference' else 'restated port, oracle/'}; "
+                         f"{m['strategy']} {m['precision']}, the reference bench default; workers={m['cores']}), "
+                         f"median of 5 after 2 warm-ups",
+               "ms_per_signal": m["seconds"] * 1e3 / sample}
 
     if rank == 0:
         line = {
-            "metric": "Morlet transform ms @N=102400,σ=8192; Msamples·scales/s; HBM GB/s vs peak",
-            "value": value, "unit": "Msamples·scales/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": (value / world) / (n / (PAPER_MS * 1e-3) / 1e6) if (n == 102400 and batch == 1) else None,
             "dtype": "f32" if w["precision"] == 0 else "f64",
             "data": "synthetic (device splitmix64 noise, bit-identical to make_test_signal)",
-            "config": {"workload": args.workload, "desc": w["desc"], "abbreviation": spec.abbreviation,
-                       "K": spec.half_width,
-                       "batch": batch, "n": n, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "l2": (f"rotating {R} input/output buffer pairs ({R * step_bytes / 2**20:.0f} MiB > L2)"
-                              if R > 1 else "step working set larger than L2"),
-                       "timing": "CUDA graph of K steps, CUDA events on the launch stream, max over ranks"
-                       if graph is not None else "K launches, CUDA events, max over ranks"},
+            "config": workload_config(args, w, spec.abbreviation, spec.half_width),
+            "timing": {"l2": ("L2 flushed before every timed step (2x L2 = 252 MiB written; outside the step's events)"
+                              if cold_flush else "step working set larger than L2 (no flush needed)"),
+                       "method": ("CUDA graph of K steps; per-step CUDA events (external event nodes) around the "
+                                  "transform on the launch stream; max over ranks") if graph is not None
+                       else "K launches with per-step CUDA events, max over ranks",
+                       "inputs": "2 distinct signals/batches alternated"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": step_bytes / launches,
                          "kernel": kernel_name(plan), "kernel_ms": kernel_ms},
-            "e2e": {"value": e2e_value, "unit": "Msamples·scales/s", "h2d_bytes_per_step": batch * n * in_es,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": batch * n * in_es,
                     "d2h_bytes_per_step": batch * n * out_es, "steps": e2e_steps,
                     "path": e2e_path},
-            "gpu_launches": args.steps * launches,
+            "gpu_launches": K * launches,
             "clocks": clk.summary(),
         }
         if cpu is not None:
@@ -513,7 +569,7 @@ def main():
     if args.workload == "scalogram":
         if args.impl == "reference":
             print(json.dumps({"impl": "reference", "unavailable": "scalogram CPU reference is hours of CPU time; "
-                              "reference arm runs the headline workload"}))
+                              "the reference arm times the headline workload"}))
             return
         return run_scalogram(args)
     w = WORKLOADS[args.workload]
@@ -526,7 +582,7 @@ def main():
                                                         strategy=P.Strategy.KernelIntegral))
 
     if args.impl == "reference":
-        run_reference(args, w, spec_of)
+        run_reference(args, w)
     else:
         run_ours(args, w, spec_of)
 

@@ -27,7 +27,13 @@ IMPULSE, CONSTANT, CHIRP, SEEDED_NOISE = 0, 1, 2, 3
 
 
 def build() -> str:
+    """The restated oracle, and the reference compiled from its own sources (oracle/ref.mk)
+    where those sources exist (elsewhere the prebuilt oracle/_ref is used)."""
     subprocess.check_call(["make", "-s", "-C", _HERE])
+    from . import ref
+
+    if ref.source_available():
+        ref.build()
     return _LIB_PATH
 
 
