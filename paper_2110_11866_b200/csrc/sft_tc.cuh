@@ -31,9 +31,11 @@
 //               into the fp64 tile carry
 //   warps 8-11  epilogue: TMEM -> swizzled staging (accumulator released) -> coalesced
 //               16-byte stores
-//   warps 12-15 loader: coalesced cp.async into a ring of padded staging rows; each
-//               thread then reads its chunk row, splits it (TF32 head / remainder) and
-//               tcgen05.st's it; warp 12 then issues the merged GEMM of the tile
+//   warps 12-15 loader: one thread stages each tile's lead and trail streams with two TMA
+//               boxes (SW128 rows of 32 samples) into a 3-slot ring; every thread then
+//               reads its chunk row (shifted by the plan's sub-16-byte stream offset),
+//               splits it (TF32 head / remainder) and tcgen05.st's it; warp 12 then
+//               issues the merged GEMM of the tile
 // Pipelines (mbarriers): TMEM X operands, chunk states and accumulators double-buffered;
 // loader staging ring; tile carry double-buffered.
 #pragma once
@@ -48,11 +50,12 @@
 namespace tck {
 
 struct Misc {
-  uint64_t xfree[2], g1done[2], dfree[2], g2done[2];
+  uint64_t xfull[2], xfree[2], g1done[2], dfree[2], sready[2], g2done[2];
+  uint64_t full[kLoadAhead + 1];  // loader ring slot: TMA boxes landed
   uint32_t tmem;
-  double2 cy[2][kMaxOrd];      // tile carry (state entering the tile), fp64, by tile parity
-  float2 wtot[2][4][kMaxOrd];  // per-warp chunk-aggregate totals (by tile parity)
+  double2 cy[2][kMaxOrd];  // tile carry (state entering the tile), fp64, by tile parity
 };
+static_assert(sizeof(Misc) <= 512, "Misc region");
 
 // (item, tile) walk shared by every role
 struct Walk {
@@ -84,12 +87,13 @@ struct Walk {
 
 // fp64 state entering the first processed tile of `item` for order p: the closed-form
 // contribution of the skipped constant warm-up tiles (0 when none are skipped)
-__device__ __forceinline__ double2 item_carry(const TcParams& P, long long item, int p) {
+__device__ __forceinline__ double2 item_carry(const TcParams& P, const unsigned char* sm, long long item, int p) {
   if (item >= P.n_items || P.skip0 == 0 || P.boundary == 0) return make_double2(0.0, 0.0);
   const long long sig = item / P.n_chunks;
   if (item - sig * P.n_chunks != 0) return make_double2(0.0, 0.0);
   const double v = static_cast<double>(__ldg(P.x + sig * P.ld_x));
-  return make_double2(v * P.g0[p].x, v * P.g0[p].y);
+  const double2 g0 = reinterpret_cast<const double2*>(sm + kZd)[2 * kMaxOrd + p];
+  return make_double2(v * g0.x, v * g0.y);
 }
 
 // Per-tile event clocks of CTA 0 for tools/tc_trace.py. Compiled in only with
@@ -105,78 +109,149 @@ __device__ __forceinline__ void trace_ev(const TcParams& P, long long gt, int ev
 
 __device__ __forceinline__ float tf32_lo(float v) { return v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
 
-__device__ __forceinline__ void cp_async4(uint32_t dst, const float* src, unsigned long long pol) {
-  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "l"(pol)
-               : "memory");
+// 4-byte cp.async (zero-filled when `zero`: nothing is read) and 16-byte cp.async
+__device__ __forceinline__ void cp_async4(uint32_t dst, const float* src, bool zero) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(zero ? 0 : 4) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+// the mbarrier counts one arrival once all of this thread's earlier cp.async have landed
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(umma::smem_u32(bar)) : "memory");
 }
 
-// bulk L2 prefetch of the samples a tile stream reads (clipped to the signal, 16-B aligned)
-__device__ __forceinline__ void prefetch_l2(const float* xs, long long j0, long long n) {
-  long long a = j0 < 0 ? 0 : j0, e = j0 + kTile > n ? n : j0 + kTile;
-  if (e <= a) return;
-  const uintptr_t pa = reinterpret_cast<uintptr_t>(xs + a) & ~uintptr_t(15);
-  const uintptr_t pe = (reinterpret_cast<uintptr_t>(xs + e) + 15) & ~uintptr_t(15);
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pa), "r"(static_cast<uint32_t>(pe - pa))
-               : "memory");
+// How a tile stream is staged (uniform over the loader threads; j0 = its first sample used,
+// a = j0 rounded down to 16 bytes):
+//  - kTma: the lead stream of an interior segment, one TMA box (the TMA engine carries
+//    only lead boxes and output stores: it moves ~32 B/clk per SM, tools/tma_lat.cu);
+//  - kCp: an interior trail segment (an L2 hit), 16-byte cp.async;
+//  - kZero / kFirst / kLast: one value everywhere (before the warm start, or the boundary
+//    value outside [0, n)): the reader writes it to TMEM directly;
+//  - kMixed: segments that straddle an edge or the warm start, or an input that is not
+//    16-byte aligned: per sample.
+enum StreamKind { kTma = 0, kCp = 1, kZero = 2, kFirst = 3, kLast = 4, kMixed = 5 };
+__device__ __forceinline__ int stream_kind(const TcParams& P, long long a, long long j0, long long jmin, bool lead) {
+  if (P.use_tma_in && a >= 0 && a >= jmin && a + kBoxRows * 32 <= P.n) {
+    if (lead && (a >> 5) + kBoxRows <= P.in_rows) return kTma;
+    return kCp;
+  }
+  const long long j1 = j0 + kTile;
+  if (j1 <= jmin) return kZero;
+  if (j0 >= jmin && j1 <= 0) return P.boundary != 0 ? kFirst : kZero;
+  if (j0 >= jmin && j0 >= P.n) return P.boundary != 0 ? kLast : kZero;
+  return kMixed;
 }
+constexpr uint32_t kValOff = kBoxBytes;  // per-stream words after the rows: x[0], x[n - 1]
 
-// Boundary segments of stage_rows (kept out of line: cold code, small hot loop)
-__device__ __noinline__ void stage_rows_edge(const TcParams& P, const float* xs, long long j0, long long jmin,
-                                             int lane, float* stg) {
+// A non-TMA stream of a tile, staged by the 128 loader threads t with cp.async only, so
+// that no thread waits on a global load here; the caller then arrives on the slot's
+// mbarrier with cp.async.mbarrier.arrive (completion tracked by the barrier):
+//  - kCp: the 129 SW128 rows, 16-byte copies;
+//  - kFirst / kLast / kMixed: thread 0 copies the boundary values x[0], x[n - 1] to the
+//    words at kValOff; kMixed also copies its in-signal samples (flat sample f = 32 rho + i
+//    of the slot is x[a + f]), 4-byte copies; fill_mixed stores the rest once they have
+//    landed: no copy ever reads a clamped address, which would serialise thousands of
+//    copies on one line.
+__device__ __forceinline__ void stage_stream(const TcParams& P, const float* xs, long long a, long long jmin, int kind,
+                                             int t, unsigned char* slot) {
+  const uint32_t s0 = umma::smem_u32(slot);
+  if (kind == kCp) {
+    for (int i = t; i < static_cast<int>(kBoxRows * 8); i += 128) {
+      const int row = i >> 3, pc = i & 7;
+      cp_async16(s0 + row * 128 + ((pc ^ (row & 7)) << 4), xs + a + 4 * i);
+    }
+    return;
+  }
+  if (kind == kZero) return;
   const long long n = P.n;
-  constexpr int kSeg = 32 * kQ;
-  if (j0 + kSeg <= jmin || (j0 >= jmin && (j0 >= n || j0 + kSeg <= 0))) {
-    float v = 0.f;
-    if (j0 + kSeg > jmin && P.boundary != 0) v = __ldg(xs + (j0 >= n ? n - 1 : 0));
-    for (int r = 0; r < 32; ++r) stg[r * kStgRow + lane] = v;
-    return;
+  if (t == 0) {
+    cp_async4(s0 + kValOff, xs, false);
+    cp_async4(s0 + kValOff + 4, xs + n - 1, false);
   }
-  float v[32];
-#pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    const long long j = j0 + kQ * r + lane;
-    v[r] = __ldg(xs + (j < 0 ? 0 : (j >= n ? n - 1 : j)));
-  }
-#pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    const long long j = j0 + kQ * r + lane;
-    if (j < jmin || (P.boundary == 0 && (j < 0 || j >= n))) v[r] = 0.f;
-    stg[r * kStgRow + lane] = v[r];
-  }
+  if (kind != kMixed) return;
+  const long long lo = (jmin > 0 ? jmin : 0) - a, hi = n - a;
+  const int f0 = static_cast<int>(lo < 0 ? 0 : lo);
+  const int f1 = static_cast<int>(hi > kBoxRows * 32 ? kBoxRows * 32 : (hi < 0 ? 0 : hi));
+  for (int f = f0 + t; f < f1; f += 128)
+    cp_async4(s0 + umma::sw128_off(static_cast<uint32_t>(f >> 5), static_cast<uint32_t>(f & 31)), xs + a + f, false);
 }
 
-// Stage one stream of this warp's 32 chunk rows: row r = samples j0 + 32 r + [0, 32),
-// lane l loads column l (warp-coalesced) into the padded staging rows. Segment classes as
-// in K1's stage_stream: inside the signal (cp.async), or a boundary segment (uniform
-// boundary value, or straddling an edge / the warm start: per element).
-__device__ __forceinline__ void stage_rows(const TcParams& P, const float* xs, long long j0, long long jmin, int lane,
-                                           unsigned long long pol, float* stg) {
-  constexpr int kSeg = 32 * kQ;
-  if (j0 >= jmin && j0 >= 0 && j0 + kSeg <= P.n) {
-    const uint32_t s0 = umma::smem_u32(stg) + 4u * static_cast<uint32_t>(lane);
-    const float* p = xs + j0 + lane;
+// a uniform stream row: the same value in every TMEM column (head and remainder)
+__device__ __forceinline__ void uniform_to_tmem(float v, uint32_t taddr) {
+  uint32_t h[16], l[16];
 #pragma unroll
-    for (int r = 0; r < 32; ++r) cp_async4(s0 + r * kStgRow * 4, p + kQ * r, pol);
-    return;
+  for (int i = 0; i < 16; ++i) {
+    h[i] = __float_as_uint(v);
+    l[i] = __float_as_uint(tf32_lo(v));
   }
-  stage_rows_edge(P, xs, j0, jmin, lane, stg);
+  umma::tmem_st16(taddr, h);
+  umma::tmem_st16(taddr + 16, h);
+  umma::tmem_st16(taddr + 32, l);
+  umma::tmem_st16(taddr + 48, l);
 }
 
-// this thread's chunk row from staging -> TMEM: head columns [col, +32), remainder [col+32, +32)
-__device__ __forceinline__ void row_to_tmem(const float* stg, int lane, uint32_t taddr) {
-  uint32_t h[32], l[32];
+// Chunk row c of a staged stream, R samples past its box start (flat samples
+// 32 c + R + [0, 32)), split into the TF32 head (the raw value: the MMA reads its head)
+// and the fp32 remainder -> TMEM columns [0, 32) head and [32, 64) remainder of taddr.
+// SW128 rows make the 16-byte row reads of 8 consecutive threads conflict-free.
+template <int R>
+__device__ __forceinline__ void row_to_tmem_r(const unsigned char* slot, int c, uint32_t taddr) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float4 v = *reinterpret_cast<const float4*>(stg + lane * kStgRow + 4 * j);
-    h[4 * j] = __float_as_uint(v.x);
-    h[4 * j + 1] = __float_as_uint(v.y);
-    h[4 * j + 2] = __float_as_uint(v.z);
-    h[4 * j + 3] = __float_as_uint(v.w);
+  for (int hh = 0; hh < 2; ++hh) {
+    float f[20];
+#pragma unroll
+    for (int k = 0; k < (R ? 5 : 4); ++k) {
+      const int p = 4 * hh + k, row = c + (p >> 3), pc = p & 7;
+      const float4 v = *reinterpret_cast<const float4*>(slot + row * 128 + ((pc ^ (row & 7)) << 4));
+      f[4 * k] = v.x;
+      f[4 * k + 1] = v.y;
+      f[4 * k + 2] = v.z;
+      f[4 * k + 3] = v.w;
+    }
+    uint32_t h[16], l[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float v = f[R + i];
+      h[i] = __float_as_uint(v);
+      l[i] = __float_as_uint(tf32_lo(v));
+    }
+    umma::tmem_st16(taddr + 16 * hh, h);
+    umma::tmem_st16(taddr + 32 + 16 * hh, l);
   }
-#pragma unroll
-  for (int i = 0; i < 32; ++i) l[i] = __float_as_uint(tf32_lo(__uint_as_float(h[i])));
-  umma::tmem_st32(taddr, h);
-  umma::tmem_st32(taddr + 32, l);
+}
+__device__ __forceinline__ void row_to_tmem(const unsigned char* slot, int r, int c, uint32_t taddr) {
+  switch (r) {  // plan-uniform
+    case 0: row_to_tmem_r<0>(slot, c, taddr); break;
+    case 1: row_to_tmem_r<1>(slot, c, taddr); break;
+    case 2: row_to_tmem_r<2>(slot, c, taddr); break;
+    default: row_to_tmem_r<3>(slot, c, taddr); break;
+  }
+}
+// kMixed stream staged from a: once its in-signal samples have landed, the loader
+// threads t store the rest of the slot (zeros before the warm start, the boundary policy
+// outside [0, n)) so that the regular row reader applies. Cold path, out of line: the
+// slot comes in as a shared-window address (a generic pointer would make every store a
+// generic one).
+__device__ __noinline__ void fill_mixed(long long n, int boundary, uint32_t slot, int t, long long a, long long jmin) {
+  auto clip = [](long long v) {
+    return static_cast<int>(v < 0 ? 0 : (v > kBoxRows * 32 ? kBoxRows * 32 : v));
+  };
+  const int fj = clip(jmin - a), f0 = clip(-a), fn = clip(n - a);
+  float v0 = 0.f, vn = 0.f;
+  if (boundary != 0) {
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v0) : "r"(slot + kValOff));
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(vn) : "r"(slot + kValOff + 4));
+  }
+  auto put = [&](int f, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(slot + umma::sw128_off(static_cast<uint32_t>(f >> 5),
+                                                                       static_cast<uint32_t>(f & 31))),
+                 "f"(v)
+                 : "memory");
+  };
+  const int fz = fj > f0 ? fj : f0;  // [0, fj) zeros (warm start), then [fj, f0) x[0]
+  for (int f = t; f < fz; f += 128) put(f, f < fj ? 0.f : v0);
+  for (int f = fn + t; f < static_cast<int>(kBoxRows * 32); f += 128) put(f, vn);
 }
 
 __device__ __noinline__ void store_masked(float* dst, float4 val, long long pos, long long cnt, int cw) {
@@ -185,7 +260,7 @@ __device__ __noinline__ void store_masked(float* dst, float4 val, long long pos,
     if (pos + j / cw < cnt) dst[j] = e[j];
 }
 
-// named barriers: scan order-sets (1, 2), epilogue (3), loader (4), all scan warps (5)
+// named barriers: epilogue (3), loader (4), scan warps (5)
 __device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __device__ __forceinline__ float2 cmla(float2 z, float2 t, float2 a) {  // a + z t
@@ -216,7 +291,9 @@ __device__ __forceinline__ void warm_k(uint64_t db, uint32_t d, uint32_t x, uint
 template <int NORD>
 __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_constant__ TcParams P) {
   extern __shared__ __align__(1024) unsigned char smraw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base, derived by pointer arithmetic on the shared array so that the
+  // compiler keeps every access in the shared window (LDS/STS, not generic LD/ST)
+  unsigned char* sm = smraw + ((1024u - (umma::smem_u32(smraw) & 1023u)) & 1023u);
   Misc& M = *reinterpret_cast<Misc*>(sm + kMisc);
   const int tid = threadIdx.x, lane = tid & 31;
   // warp index as a provably warp-uniform value: role branches become uniform branches
@@ -231,14 +308,18 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
   }
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&M.xfull[b], 128);
       umma::mbar_init(&M.xfree[b], 1);
       umma::mbar_init(&M.g1done[b], 1);
       umma::mbar_init(&M.dfree[b], 128);
+      umma::mbar_init(&M.sready[b], 256);
       umma::mbar_init(&M.g2done[b], 1);
     }
+    for (int k = 0; k <= kLoadAhead; ++k) umma::mbar_init(&M.full[k], 129);  // TMA issuer + 128 cp.async arrivals
     umma::mbar_fence_init();
   }
-  if (tid < kMaxOrd) M.cy[0][tid] = item_carry(P, blockIdx.x, tid);
+  __syncthreads();  // image (g0) in shared memory
+  if (tid < kMaxOrd) M.cy[0][tid] = item_carry(P, sm, blockIdx.x, tid);
   if (warp == 0) umma::tmem_alloc(&M.tmem, 512);
   umma::fence_proxy_async();
   umma::fence_before();
@@ -246,93 +327,185 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
   umma::fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, M.tmem, 0);  // warp-uniform
   constexpr int nord = NORD;
-  const uint64_t dbase = umma::desc_sw128(umma::smem_u32(sm));
 
-  if (warp >= 12) {
-    // ================= loader: warp q owns chunk rows [32 q, +32) = TMEM lanes of warp q
-    const int q = warp - 12;
-    const uint32_t lrow = static_cast<uint32_t>(q * 32) << 16;
-    float* const stg = reinterpret_cast<float*>(sm + kLStage + q * kStgWarp);
-    unsigned long long keep, first;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(first));
+  if (warp == 16) {
+    // ================= MMA issuer: merged GEMM of tile gt, then the chunk-state GEMM of
+    // the previous output tile (issued after it so that it overlaps that tile's scan)
+    const uint64_t dbase = umma::desc_sw128(umma::smem_u32(sm));
     const uint32_t idm = umma::idesc_tf32(128, NO + 16), ida = umma::idesc_tf32(128, 16);
-    auto issue = [&](const Walk& w, int buf) {
-      if (w.valid) {
-        const float* xs = P.x + w.sig * P.ld_x;
-        const long long lo = P.lo + w.obase, o0 = w.o0(P) + 32LL * kQ * q, jmin = lo - P.K;
-        float* sb = stg + buf * 2 * 32 * kStgRow;
-        stage_rows(P, xs, lo + o0 + P.K, jmin, lane, keep, sb);
-        if (!w.warm(P)) stage_rows(P, xs, lo + o0 - P.K, jmin, lane, first, sb + 32 * kStgRow);
-        if (lane == 0) {
-          Walk nx = w;
-          nx.advance(P);
-          if (nx.valid) {
-            const float* xn = P.x + nx.sig * P.ld_x;
-            const long long ln = P.lo + nx.obase, on = nx.o0(P) + 32LL * kQ * q;
-            prefetch_l2(xn, ln + on + P.K, P.n);
-            if (!nx.warm(P)) prefetch_l2(xn, ln + on - P.K, P.n);
+    const uint32_t ids = umma::idesc_tf32(128, NO);
+    long long u = 0;       // output tiles whose state GEMM has been issued
+    int pend = -1;         // accumulator of the output tile whose state GEMM is pending
+    auto state_gemm = [&]() {
+      const int s = static_cast<int>(u & 1);
+      umma::mbar_wait(&M.sready[s], static_cast<uint32_t>((u >> 1) & 1));
+      umma::fence_after();
+      const uint32_t d = tmem + (pend ? kTD1 : kTD0), a = tmem + kTSS + 32 * s;
+      umma::mma_tf32_ts<kBC>(d, a, dbase, ids, 1);  // S_h . C_h
+      umma::mma_tf32_ts<kBC + 32>(d, a + 8, dbase, ids, 1);
+      umma::mma_tf32_ts<kBC>(d, a + 16, dbase, ids, 1);  // S_l . C_h
+      umma::mma_tf32_ts<kBC + 32>(d, a + 24, dbase, ids, 1);
+      umma::mma_tf32_ts<kBC + 64>(d, a, dbase, ids, 1);  // S_h . C_l
+      umma::mma_tf32_ts<kBC + 96>(d, a + 8, dbase, ids, 1);
+      umma::commit_elect(&M.g2done[s]);
+      ++u;
+      pend = -1;
+    };
+    Walk w;
+    w.begin(P);
+    for (long long gt = 0; w.valid; ++gt) {
+      const int b = static_cast<int>(gt & 1);
+      const bool warm = w.warm(P);
+      const uint32_t xph = static_cast<uint32_t>((gt >> 1) & 1), dph = static_cast<uint32_t>(((gt >> 1) - 1) & 1);
+      if (pend >= 0) {
+        // the previous output tile's state GEMM goes first if its states are ready before
+        // this tile's operands (it gates that tile's epilogue and accumulator release)
+        const int s = static_cast<int>(u & 1);
+        const uint32_t sph = static_cast<uint32_t>((u >> 1) & 1);
+        bool xok = false;
+        for (;;) {
+          if (umma::mbar_test(&M.sready[s], sph)) {
+            state_gemm();
+            if (lane == 0) trace_ev(P, gt - 1, 5);
+            break;
           }
+          if (!xok) xok = umma::mbar_test(&M.xfull[b], xph) && (gt < 2 || umma::mbar_test(&M.dfree[b], dph));
+          if (xok) break;
         }
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");  // one group per tile (possibly empty)
+      umma::mbar_wait(&M.xfull[b], xph);
+      if (gt >= 2) umma::mbar_wait(&M.dfree[b], dph);
+      umma::fence_after();
+      if (lane == 0) trace_ev(P, gt, 1);
+      const uint32_t d = tmem + (b ? kTD1 : kTD0), x = tmem + kTX + 128 * b;
+      if (!warm) {
+        merged_k<0>(dbase, d, x, idm);
+        merged_k<1>(dbase, d, x, idm);
+        merged_k<2>(dbase, d, x, idm);
+        merged_k<3>(dbase, d, x, idm);
+      } else if (NO == 64) {
+        warm_k<0, 64>(dbase, d + 64, x, ida);
+        warm_k<1, 64>(dbase, d + 64, x, ida);
+        warm_k<2, 64>(dbase, d + 64, x, ida);
+        warm_k<3, 64>(dbase, d + 64, x, ida);
+      } else {
+        warm_k<0, 32>(dbase, d + 32, x, ida);
+        warm_k<1, 32>(dbase, d + 32, x, ida);
+        warm_k<2, 32>(dbase, d + 32, x, ida);
+        warm_k<3, 32>(dbase, d + 32, x, ida);
+      }
+      umma::commit_elect(&M.g1done[b]);
+      umma::commit_elect(&M.xfree[b]);
+      if (lane == 0) trace_ev(P, gt, 2);
+      if (pend >= 0) {
+        state_gemm();
+        if (lane == 0) trace_ev(P, gt - 1, 5);
+      }
+      if (!warm) pend = b;
+      w.advance(P);
+    }
+    if (pend >= 0) state_gemm();
+  } else if (warp >= 12) {
+    // ================= loader: thread t = chunk row t = TMEM lane t (warp q: lanes [32 q, +32))
+    const int q = warp - 12, t = tid - 384;
+    const uint32_t lrow = static_cast<uint32_t>(q * 32) << 16;
+    unsigned char* const leads = sm + kLStage;
+    unsigned char* const trails = sm + kTrail;
+    unsigned long long keep;  // lead lines are read again 2K positions later as the trail
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+    if (P.dbg & 2) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(keep));
+    // stream starts of a tile: lead x[n + K], trail x[n - K] from n = lo + o0, each
+    // rounded down to 16 bytes (rl / rt samples before the first one used)
+    auto starts = [&](const Walk& w, long long& al, long long& at, long long& jmin) {
+      const long long lo = P.lo + w.obase, o0 = w.o0(P);
+      jmin = lo - P.K;
+      al = lo + o0 + P.K - P.rl;
+      at = lo + o0 - P.K - P.rt;
+    };
+    // stage tile w into ring slot `slot`: the lead box by TMA (one thread, transaction
+    // bytes on full[slot]), everything else by cp.async from all 128 loader threads; every
+    // loader thread then arrives on full[slot] once its copies have landed (129 arrivals)
+    auto kinds = [&](const Walk& w, long long al, long long at, long long jmin, int& kl, int& kt) {
+      kl = stream_kind(P, al, al + P.rl, jmin, true);
+      kt = w.warm(P) ? kZero : stream_kind(P, at, at + P.rt, jmin, false);
+    };
+    auto issue = [&](const Walk& w, int slot, long long gtrace) {
+      if (!w.valid) return;
+      long long al, at, jmin;
+      starts(w, al, at, jmin);
+      int kl, kt;
+      kinds(w, al, at, jmin, kl, kt);
+      unsigned char* const sl = leads + slot * kLeadBytes;
+      unsigned char* const st = trails + slot * kTrailBytes;
+      if (t == 0) {
+        trace_ev(P, gtrace, 13);
+        umma::mbar_arrive_tx(&M.full[slot], kl == kTma ? kBoxBytes : 0u);
+        if (kl == kTma)
+          umma::tma_load_3d(umma::smem_u32(sl), &P.in_map, &M.full[slot], static_cast<int>(al & 31),
+                            static_cast<int>(al >> 5), static_cast<int>(w.sig), keep);
+      }
+      const float* xs = P.x + w.sig * P.ld_x;
+      if (kl != kTma) stage_stream(P, xs, al, jmin, kl, t, sl);
+      stage_stream(P, xs, at, jmin, kt, t, st);
+      cp_async_arrive(&M.full[slot]);
     };
     // staging ring of kLoadAhead + 1 tiles: tile gt + kLoadAhead is issued before tile gt
-    // is moved into TMEM
+    // is moved into TMEM (its slot was last read by tile gt - 1, before its bar 4)
+    uint32_t fph = 0;  // full[] phase bits
     Walk wi, w;
     wi.begin(P);
     w.begin(P);
     for (int k = 0; k < kLoadAhead; ++k) {
-      issue(wi, k);
+      issue(wi, k, k);
       if (wi.valid) wi.advance(P);
     }
     for (long long gt = 0; w.valid; ++gt) {
-      issue(wi, static_cast<int>((gt + kLoadAhead) % (kLoadAhead + 1)));
+      issue(wi, static_cast<int>((gt + kLoadAhead) % (kLoadAhead + 1)), gt + kLoadAhead);
       if (wi.valid) wi.advance(P);
-      asm volatile("cp.async.wait_group %0;" ::"n"(kLoadAhead) : "memory");
-      __syncwarp();
+      if (t == 0) trace_ev(P, gt, 11);
+      const int slot = static_cast<int>(gt % (kLoadAhead + 1));
+      const bool warm = w.warm(P);
+      int kl, kt;
+      long long al, at, jmin;
+      starts(w, al, at, jmin);
+      kinds(w, al, at, jmin, kl, kt);
+      umma::mbar_wait(&M.full[slot], (fph >> slot) & 1u);
+      fph ^= 1u << slot;
+      umma::fence_proxy_async();  // the cp.async writes precede a later TMA box in this slot
+      if (t == 0) trace_ev(P, gt, 10);
       const int b = static_cast<int>(gt & 1);
       if (gt >= 2) umma::mbar_wait(&M.xfree[b], static_cast<uint32_t>(((gt >> 1) - 1) & 1));
       __syncwarp();
       umma::fence_after();
-      if (lane == 0) trace_ev(P, gt, 0);
-      const float* sb = stg + static_cast<int>(gt % (kLoadAhead + 1)) * 2 * 32 * kStgRow;
+      if (t == 0) trace_ev(P, gt, 0);
+      const unsigned char* sl = leads + slot * kLeadBytes;
+      const unsigned char* st = trails + slot * kTrailBytes;
       const uint32_t tx = tmem + lrow + kTX + 128 * b;
-      const bool warm = w.warm(P);
-      row_to_tmem(sb, lane, tx);
-      if (!warm) row_to_tmem(sb + 32 * kStgRow, lane, tx + 64);
+      // uniform streams: zero, x[0] (kFirst) or x[n - 1] (kLast)
+      auto uval = [&](const unsigned char* p, int k) {
+        return k == kZero ? 0.f : *reinterpret_cast<const float*>(p + kValOff + (k == kLast ? 4 : 0));
+      };
+      if (t == 0) trace_ev(P, gt, 15);
+      if (kl == kMixed || kt == kMixed) {
+        if (kl == kMixed) fill_mixed(P.n, P.boundary, umma::smem_u32(sl), t, al, jmin);
+        if (kt == kMixed) fill_mixed(P.n, P.boundary, umma::smem_u32(st), t, at, jmin);
+        bar_named(4, 128);
+      }
+      if (kl == kTma || kl == kCp || kl == kMixed)
+        row_to_tmem(sl, P.rl, t, tx);
+      else
+        uniform_to_tmem(uval(sl, kl), tx);
+      if (t == 0) trace_ev(P, gt, 12);
+      if (!warm) {
+        if (kt == kTma || kt == kCp || kt == kMixed)
+          row_to_tmem(st, P.rt, t, tx + 64);
+        else
+          uniform_to_tmem(uval(st, kt), tx + 64);
+      }
       umma::tmem_wait_st();
       umma::fence_before();
-      bar_named(4, 128);  // all four lane quarters of the tile are in TMEM
-      if (lane == 0) trace_ev(P, gt, 1);
-      if (q == 0) {
-        // merged GEMM (outputs + aggregates; warm tiles: aggregates of the lead stream)
-        // into accumulator b once the epilogue / scan have released it
-        if (gt >= 2) umma::mbar_wait(&M.dfree[b], static_cast<uint32_t>(((gt >> 1) - 1) & 1));
-        __syncwarp();
-        umma::fence_after();
-        const uint32_t d = tmem + (b ? kTD1 : kTD0), x = tmem + kTX + 128 * b;
-        if (!warm) {
-          merged_k<0>(dbase, d, x, idm);
-          merged_k<1>(dbase, d, x, idm);
-          merged_k<2>(dbase, d, x, idm);
-          merged_k<3>(dbase, d, x, idm);
-        } else if (NO == 64) {
-          warm_k<0, 64>(dbase, d + 64, x, ida);
-          warm_k<1, 64>(dbase, d + 64, x, ida);
-          warm_k<2, 64>(dbase, d + 64, x, ida);
-          warm_k<3, 64>(dbase, d + 64, x, ida);
-        } else {
-          warm_k<0, 32>(dbase, d + 32, x, ida);
-          warm_k<1, 32>(dbase, d + 32, x, ida);
-          warm_k<2, 32>(dbase, d + 32, x, ida);
-          warm_k<3, 32>(dbase, d + 32, x, ida);
-        }
-        umma::commit_elect(&M.g1done[b]);
-        umma::commit_elect(&M.xfree[b]);
-        if (lane == 0) trace_ev(P, gt, 2);
-      }
-      __syncwarp();  // every lane has read its row before the ring slot is refilled
+      umma::mbar_arrive(&M.xfull[b]);
+      bar_named(4, 128);  // every row of the slot has been read: it may be refilled
       w.advance(P);
     }
   } else if (warp >= 8) {
@@ -379,9 +552,17 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
         bar_named(3, 128);
         if (c == 0) {
           const int row0 = static_cast<int>((w.obase + o0) / kQ), sg = static_cast<int>(w.sig);
+          unsigned long long spol;
+          asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(spol));
           for (int h = 0; h < halves; ++h) {
             const uint32_t src = umma::smem_u32(stgo + h * 16384);
-            if (P.cplx)
+            if (P.cplx && (P.dbg & 4))
+              asm volatile(
+                  "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4}], [%5], %6;" ::"l"(
+                      reinterpret_cast<uint64_t>(&P.out_map)),
+                  "r"(0), "r"(h), "r"(row0), "r"(sg), "r"(src), "l"(spol)
+                  : "memory");
+            else if (P.cplx)
               asm volatile(
                   "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
                       reinterpret_cast<uint64_t>(&P.out_map)),
@@ -417,14 +598,29 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     }
     if (c == 0 && P.use_tma) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else {
-    // ================= chunk-state scan: thread = chunk = TMEM lane; order set `os`
-    constexpr int hA = 4;  // set 0: orders [0, 4) (state columns 0-7), set 1: [4, 8) (8-15)
+    // ================= chunk-state scan (warps 0-7), in three phases per tile:
+    //  (1) chunk threads (thread = chunk = TMEM lane; warps 0-3 orders 0-3, warps 4-7
+    //      orders 4-7) copy the chunk aggregates A_p[c] from the accumulator into shared
+    //      memory, order-major;
+    //  (2) warp p scans order p over the tile's 128 chunks: lane t owns chunks 4t..4t+3
+    //      (a serial 4-step recurrence), plus one 5-step warp scan with multiplier
+    //      z^128 (12 shuffles per order and tile instead of a 5-step scan per chunk);
+    //      lane 31 also advances the fp64 tile carry;
+    //  (3) chunk threads move their states (TF32 head / remainder) into TMEM and signal
+    //      the MMA issuer (sready), which runs the chunk-state GEMM.
     const int os = warp >> 2;
-    const int sw = warp & 3;   // lane quarter
-    const int p0 = os ? hA : 0;
-    const int st = tid & 127;
-    const float2* zl = reinterpret_cast<const float2*>(sm + kZl);
+    const int sw = warp & 3;  // lane quarter
+    const int p0 = os * 4;
+    const int c = sw * 32 + lane;  // chunk of phases (1) and (3)
     const uint32_t lrow = static_cast<uint32_t>(sw * 32) << 16;
+    // [order][128]: aggregates, overwritten in place by the states (phase 2: each lane
+    // reads its four chunks' aggregates before it writes their states)
+    float2* const At = reinterpret_cast<float2*>(sm + kScr);
+    float2* const St = At;
+    const float2* const zs = reinterpret_cast<const float2*>(sm + kZs);     // [order][8]
+    const double2* const zd = reinterpret_cast<const double2*>(sm + kZd);   // z^4096 [order], g0
+    const float2* const z128 = reinterpret_cast<const float2*>(sm + kZ128);  // [order][32]
+    const int p = warp;  // order of phase (2)
     Walk w;
     w.begin(P);
     long long u = 0;
@@ -435,94 +631,69 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       __syncwarp();
       umma::fence_after();
       const bool warm = w.warm(P);
-      uint32_t a8[8];
-      umma::tmem_ld8(tmem + lrow + (b ? kTD1 : kTD0) + NO + 2 * p0, a8);  // this set's orders
-      umma::tmem_wait_ld();
-      if (tid == 0) trace_ev(P, gt, 8);
-      if (warm) {
-        // nothing else reads this accumulator: hand it back once both sets have read it
-        umma::fence_before();
-        bar_named(5, 256);
-        if (warp == 0) {
-          __syncwarp();
-          if (lane == 0) umma::mbar_arrive_cnt(&M.dfree[b], 128);
-        }
+      {
+        uint32_t a8[8];
+        umma::tmem_ld8(tmem + lrow + (b ? kTD1 : kTD0) + NO + 2 * p0, a8);  // this set's orders
+        umma::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (p0 + j < nord) At[(p0 + j) * kNC + c] = make_float2(__uint_as_float(a8[2 * j]), __uint_as_float(a8[2 * j + 1]));
       }
-      float2 inc[4];
-      if (warm) {
-        // only the tile total is needed: sum_l z^{32 (31 - l)} A[l] per warp
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int p = p0 + j;
-          if (j < hA && p < nord) {
-            const float2 a = make_float2(__uint_as_float(a8[2 * j]), __uint_as_float(a8[2 * j + 1]));
-            float2 s = cmla(zl[p * 32 + 31 - lane], a, make_float2(0.f, 0.f));
-#pragma unroll
-            for (int d = 16; d >= 1; d >>= 1) {
-              s.x += __shfl_xor_sync(0xffffffffu, s.x, d);
-              s.y += __shfl_xor_sync(0xffffffffu, s.y, d);
-            }
-            if (lane == 0) M.wtot[b][sw][p] = s;
-          }
-        }
-      } else {
-        // inclusive warp scan over chunks: I[l] = sum_{l' <= l} z^{32 (l - l')} A[l']
-#pragma unroll
-        for (int j = 0; j < 4; ++j) inc[j] = make_float2(__uint_as_float(a8[2 * j]), __uint_as_float(a8[2 * j + 1]));
+      umma::fence_before();
+      bar_named(5, 256);
+      if (tid == 0) trace_ev(P, gt, 8);
+      if (warm && tid == 0) umma::mbar_arrive_cnt(&M.dfree[b], 128);  // nothing else reads it
+      if (p < nord) {
+        const float2 z32 = zs[p * 8];
+        const float4 a01 = *reinterpret_cast<const float4*>(At + p * kNC + 4 * lane);
+        const float4 a23 = *reinterpret_cast<const float4*>(At + p * kNC + 4 * lane + 2);
+        const float2 a0 = make_float2(a01.x, a01.y), a1 = make_float2(a01.z, a01.w);
+        const float2 a2 = make_float2(a23.x, a23.y), a3 = make_float2(a23.z, a23.w);
+        // group total: sum_j z^{32 (3 - j)} a_j
+        float2 g = cmla(z32, cmla(z32, cmla(z32, a0, a1), a2), a3);
+        // inclusive warp scan over groups, multiplier z^{128 2^k}
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
           const int d = 1 << k;
-          float2 t[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (j < hA && p0 + j < nord)
-              t[j] = make_float2(__shfl_up_sync(0xffffffffu, inc[j].x, d), __shfl_up_sync(0xffffffffu, inc[j].y, d));
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (j < hA && p0 + j < nord && lane >= d) inc[j] = cmla(P.zs[p0 + j][k], t[j], inc[j]);
+          const float2 tt = make_float2(__shfl_up_sync(0xffffffffu, g.x, d), __shfl_up_sync(0xffffffffu, g.y, d));
+          if (lane >= d) g = cmla(zs[p * 8 + 1 + k], tt, g);
+        }
+        // fp64 tile carry C (state entering the tile); state entering chunk 4t:
+        // sum of the earlier groups (exclusive scan) + z^{128 t} C
+        const double2 C = M.cy[b][p];
+        float2 e = make_float2(__shfl_up_sync(0xffffffffu, g.x, 1), __shfl_up_sync(0xffffffffu, g.y, 1));
+        if (lane == 0) e = make_float2(0.f, 0.f);
+        if (!warm) {
+          const float2 zc = z128[p * 32 + lane];
+          const float2 cf = make_float2(static_cast<float>(C.x), static_cast<float>(C.y));
+          const float2 cz = cmla(zc, cf, make_float2(0.f, 0.f));
+          const float2 s0 = make_float2(e.x + cz.x, e.y + cz.y);
+          const float2 s1 = cmla(z32, s0, a0), s2 = cmla(z32, s1, a1), s3 = cmla(z32, s2, a2);
+          *reinterpret_cast<float4*>(St + p * kNC + 4 * lane) = make_float4(s0.x, s0.y, s1.x, s1.y);
+          *reinterpret_cast<float4*>(St + p * kNC + 4 * lane + 2) = make_float4(s2.x, s2.y, s3.x, s3.y);
         }
         if (lane == 31) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (j < hA && p0 + j < nord) M.wtot[b][sw][p0 + j] = inc[j];
+          // carry into the next tile (fp64): z^{4096} C + (tile total)
+          const double2 zt = zd[p];
+          M.cy[b ^ 1][p] = w.last(P) ? item_carry(P, sm, w.item + gridDim.x, p)
+                                     : make_double2(fma(zt.x, C.x, fma(-zt.y, C.y, static_cast<double>(g.x))),
+                                                    fma(zt.x, C.y, fma(zt.y, C.x, static_cast<double>(g.y))));
         }
       }
+      bar_named(5, 256);  // states in shared memory; At / St free for the next tile after phase 3
       if (tid == 0) trace_ev(P, gt, 9);
-      bar_named(1 + os, 128);
-      if (tid == 0) trace_ev(P, gt, 11);
-      const double2* cyin = M.cy[b];
       if (!warm) {
-        // state entering chunk c: S = excl + z^{32 lane} W_warp. Lane j < set size derives
-        // W_warp for order p0 + j from the fp64 tile carry and the earlier warps' totals.
-        float2 Wp = make_float2(0.f, 0.f);
-        if (lane < hA && p0 + lane < nord) {
-          const int p = p0 + lane;
-          const double2 z = P.z1024[p];
-          double2 Wd = cyin[p];
-          for (int w2 = 0; w2 < sw; ++w2) {
-            const float2 t = M.wtot[b][w2][p];
-            Wd = make_double2(fma(z.x, Wd.x, fma(-z.y, Wd.y, static_cast<double>(t.x))),
-                              fma(z.x, Wd.y, fma(z.y, Wd.x, static_cast<double>(t.y))));
-          }
-          Wp = make_float2(static_cast<float>(Wd.x), static_cast<float>(Wd.y));
-        }
         uint32_t sh[8], sl[8];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           float2 s = make_float2(0.f, 0.f);
-          if (j < hA && p0 + j < nord) {
-            const float2 W = make_float2(__shfl_sync(0xffffffffu, Wp.x, j), __shfl_sync(0xffffffffu, Wp.y, j));
-            float2 e = make_float2(__shfl_up_sync(0xffffffffu, inc[j].x, 1), __shfl_up_sync(0xffffffffu, inc[j].y, 1));
-            if (lane == 0) e = make_float2(0.f, 0.f);
-            s = cmla(zl[(p0 + j) * 32 + lane], W, e);
-          }
+          if (p0 + j < nord) s = St[(p0 + j) * kNC + c];
           // head = the raw value (the MMA reads its TF32 head), remainder separately
           sh[2 * j] = __float_as_uint(s.x);
           sh[2 * j + 1] = __float_as_uint(s.y);
           sl[2 * j] = __float_as_uint(tf32_lo(s.x));
           sl[2 * j + 1] = __float_as_uint(tf32_lo(s.y));
         }
-        if (tid == 0) trace_ev(P, gt, 12);
         // this state buffer is free once the chunk-state GEMM of output tile u-2 is done
         const int s = static_cast<int>(u & 1);
         if (u >= 2) umma::mbar_wait(&M.g2done[s], static_cast<uint32_t>(((u >> 1) - 1) & 1));
@@ -533,38 +704,9 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
         umma::tmem_st8(ts + 16, sl);
         umma::tmem_wait_st();
         umma::fence_before();
-        bar_named(5, 256);  // both order sets' states are in TMEM
+        umma::mbar_arrive(&M.sready[s]);
         if (tid == 0) trace_ev(P, gt, 4);
-        if (warp == 0) {
-          // chunk-state GEMM: D[:, 0:NO) += S . C^T (3xTF32)
-          umma::fence_after();
-          const uint32_t d = tmem + (b ? kTD1 : kTD0), a = tmem + kTSS + 32 * s;
-          const uint32_t ids = umma::idesc_tf32(128, NO);
-          umma::mma_tf32_ts<kBC>(d, a, dbase, ids, 1);  // S_h . C_h
-          umma::mma_tf32_ts<kBC + 32>(d, a + 8, dbase, ids, 1);
-          umma::mma_tf32_ts<kBC>(d, a + 16, dbase, ids, 1);  // S_l . C_h
-          umma::mma_tf32_ts<kBC + 32>(d, a + 24, dbase, ids, 1);
-          umma::mma_tf32_ts<kBC + 64>(d, a, dbase, ids, 1);  // S_h . C_l
-          umma::mma_tf32_ts<kBC + 96>(d, a + 8, dbase, ids, 1);
-          umma::commit_elect(&M.g2done[s]);
-          if (lane == 0) trace_ev(P, gt, 5);
-        }
         ++u;
-      }
-      if (st < hA && p0 + st < nord && sw == 0) {
-        // carry into the next tile (fp64): z^{4096} C + sum_w z^{1024 (3 - w)} T_w
-        const int p = p0 + st;
-        const double2 z = P.z1024[p], zt = P.zT[p];
-        double2 T = make_double2(0.0, 0.0);
-        for (int w2 = 0; w2 < 4; ++w2) {
-          const float2 t = M.wtot[b][w2][p];
-          T = make_double2(fma(z.x, T.x, fma(-z.y, T.y, static_cast<double>(t.x))),
-                           fma(z.x, T.y, fma(z.y, T.x, static_cast<double>(t.y))));
-        }
-        const double2 cy = cyin[p];
-        M.cy[b ^ 1][p] = w.last(P) ? item_carry(P, w.item + gridDim.x, p)
-                                   : make_double2(fma(zt.x, cy.x, fma(-zt.y, cy.y, T.x)),
-                                                  fma(zt.x, cy.y, fma(zt.y, cy.x, T.y)));
       }
       w.advance(P);
     }

@@ -13,44 +13,63 @@ constexpr int kQ = 32;           // positions per chunk (GEMM K per stream)
 constexpr int kNC = 128;         // chunks per tile (GEMM M)
 constexpr int kTile = kQ * kNC;  // 4096 positions
 constexpr int kMaxOrd = 8;       // 2 * orders <= 16 aggregate columns
-constexpr int kThreads = 512;    // 16 warps: scan (2 order sets), epilogue, loader
+constexpr int kThreads = 544;    // 17 warps: scan (8), epilogue (4), loader (4), MMA issuer (1)
 
 // shared-memory image (bytes; SW128 K-major B operands, 1024-aligned regions).
 // BL/BT: [output rows (NO = 64 complex / 32 real) ; 16 aggregate rows] x 32 positions for
 // the lead / trail streams, TF32 head (h) and remainder (l); BC: chunk-state -> output,
 // columns [C head (16) | C remainder (16)].
 constexpr uint32_t kBLh = 0, kBLl = 10240, kBTh = 20480, kBTl = 30720, kBC = 40960;
-constexpr uint32_t kZl = 49152;     // float2 [kMaxOrd][32]: z^{32 l}
-constexpr uint32_t kImage = 51200;  // bytes copied from the plan's device image
-constexpr uint32_t kStgRow = 36;    // padded staging row (floats): conflict-free row reads
-constexpr int kLoadAhead = 2;       // loader lookahead (tiles in flight ahead of the one stored)
-constexpr uint32_t kStgWarp = (kLoadAhead + 1) * 2 * 32 * kStgRow * 4;  // [ring slot][stream][32 rows]
-constexpr uint32_t kLStage = kImage;                     // loader staging, 4 warps
-constexpr uint32_t kStage = kLStage + 4 * kStgWarp;      // epilogue staging (128 rows x 128 B)
-constexpr uint32_t kMisc = kStage + 32768;  // epilogue staging: two halves
-constexpr uint32_t kSmemBytes = kMisc + 1024 + 1024;  // misc + alignment slack
+// Per-order scan constants in shared memory (the scan indexes them by order / lane):
+constexpr uint32_t kZ128 = 49152;   // float2 [kMaxOrd][32]: z^{128 t}
+constexpr uint32_t kZs = 51200;     // float2 [kMaxOrd][8]: z^{32}, z^{128 * 2^k} (k < 5)
+constexpr uint32_t kZd = 51712;     // double2 [3][kMaxOrd]: z^{4096}, (unused), g0
+constexpr uint32_t kImage = 52096;  // bytes copied from the plan's device image
+// Loader staging: a ring of kLoadAhead + 1 tiles. Each tile stream is 129 SW128 rows of
+// 32 samples (row rho, column i = sample a + 32 rho + i, a = the stream's first sample
+// rounded down to 16 bytes; the 129th row carries the <= 3 samples a misaligned stream
+// spills past 4096), followed by one word for a uniform stream's value. Lead streams are
+// TMA boxes (1024-aligned destinations); trail streams are cp.async'd (128-aligned).
+constexpr int kLoadAhead = 3;                    // tiles in flight ahead of the one moved to TMEM
+constexpr uint32_t kBoxRows = kNC + 1;           // 129 rows per stream
+constexpr uint32_t kBoxBytes = kBoxRows * 128;   // 16512 bytes of TMA transaction per lead box
+constexpr uint32_t kLeadBytes = 17408;           // lead stride (1024-aligned)
+constexpr uint32_t kTrailBytes = 16640;          // trail stride (rows + value word, 128-aligned)
+constexpr uint32_t kLStage = (kImage + 1023) / 1024 * 1024;                 // lead ring
+constexpr uint32_t kTrail = kLStage + (kLoadAhead + 1) * kLeadBytes;       // trail ring
+constexpr uint32_t kStage = kTrail + (kLoadAhead + 1) * kTrailBytes;       // epilogue staging (SW128)
+constexpr uint32_t kScr = kStage + 32768;  // epilogue staging: two halves; then the scan's
+                                           // aggregates / states [order][chunk] (aliased)
+constexpr uint32_t kMisc = kScr + kMaxOrd * kNC * 8;
+constexpr uint32_t kSmemBytes = kMisc + 512 + 1024;  // misc + alignment slack
+static_assert(kStage % 1024 == 0 && kLStage % 1024 == 0, "SW128 regions need 1024-byte alignment");
+static_assert(kSmemBytes <= 232448, "shared memory budget (227 KB)");
 // TMEM columns (512 allocated): X operands [stage][xl_h, xl_l, xt_h, xt_l] x 32,
 // chunk states [2][S_h (16) | S_l (16)], accumulators [2][outputs | aggregates]
 constexpr uint32_t kTX = 0, kTSS = 256, kTD0 = 320, kTD1 = 416;
 
 struct TcParams {
   CUtensorMap out_map;  // TMA view of the output (see run_tc); valid when use_tma
+  // TMA view of the input for the loader: [signal][row][64 samples], rows 32 samples
+  // (128 B) apart, so a box of 32 samples may start at any 16-byte aligned sample
+  // (overlapping rows); valid when use_tma_in
+  CUtensorMap in_map;
+  long long in_rows;  // rows of in_map (row r + 1 of a box must lie below in_rows)
   const float* x;
   float* out;
   long long n, ld_x, ld_out;  // ld_out in outputs (complex outputs count once)
   long long lo, count;        // first output position, outputs per signal
   long long chunk_len, n_chunks, n_items, warm_tiles;
-  int K, boundary, nord, cplx, vec_ok, use_tma;
+  int K, boundary, nord, cplx, vec_ok, use_tma, use_tma_in;
+  int rl, rt;  // (lo + K) mod 4, (lo - K) mod 4: sample offsets of the lead / trail streams
+               // from their 16-byte aligned box starts (uniform over the plan)
   const uint4* image;  // kImage bytes
   long long* trace;    // optional: per-tile event clocks of CTA 0 ([64][8]), tools/tc_trace.py
-  float2 zs[kMaxOrd][6];  // z^{32 * 2^k} (k < 5), z^{1024}
-  double2 z1024[kMaxOrd];
-  double2 zT[kMaxOrd];  // z^{4096}
   // Leading warm-up tiles of a signal's first chunk whose lead samples all lie in the
   // uniform boundary region (before sample 0) are not processed: the state they build is
   // v * g0[p], v = x[0] (clamp) or 0 (zero boundary), g0 = sum_{e < E} z^e (host, fp64).
-  int skip0;
-  double2 g0[kMaxOrd];
+  int skip0;  // g0 lives in the image (kZd)
+  int dbg;    // experiment switches (SFTGPU_TC_DBG): 2 no lead L2 hint, 4 evict-first output stores
 };
 
 cudaError_t launch_tc(const TcParams& p, int grid, cudaStream_t s);

@@ -140,6 +140,8 @@ struct sftgpu_plan {
   int tc_grid = 0;
   const void* tc_map_out = nullptr;  // output buffer the cached TMA map describes
   long long tc_map_ld = -1;
+  const void* tc_map_in = nullptr;  // input buffer the cached loader map describes
+  long long tc_map_in_ld = -1;
   // pipelined host execution: internal copy-in / compute / copy-out streams and a ring
   // of staging slots, so the transfers of neighbouring calls overlap this call's kernel
   struct Slot {
@@ -605,26 +607,20 @@ bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
   std::memset(&P, 0, sizeof(P));
   for (int p = 0; p < nord; ++p) {
     const double w = ords[p].omega;
-    for (int l = 0; l < 32; ++l) {
-      const cd v = zpow(alpha, w, 32.0 * l);
-      const float f[2] = {static_cast<float>(v.real()), static_cast<float>(v.imag())};
-      std::memcpy(&img[tck::kZl + (p * 32 + l) * 8], f, 8);
+    for (int t = 0; t < 32; ++t) {
+      const cd v = zpow(alpha, w, 128.0 * t);
+      const float f2[2] = {static_cast<float>(v.real()), static_cast<float>(v.imag())};
+      std::memcpy(&img[tck::kZ128 + (p * 32 + t) * 8], f2, 8);
     }
     for (int k = 0; k < 6; ++k) {
-      const cd v = zpow(alpha, w, k < 5 ? 32.0 * (1 << k) : 1024.0);
-      P.zs[p][k] = make_float2(static_cast<float>(v.real()), static_cast<float>(v.imag()));
+      const cd v = zpow(alpha, w, k == 0 ? 32.0 : 128.0 * (1 << (k - 1)));
+      const float f2[2] = {static_cast<float>(v.real()), static_cast<float>(v.imag())};
+      std::memcpy(&img[tck::kZs + (p * 8 + k) * 8], f2, 8);
     }
-    const cd z1 = zpow(alpha, w, 1024.0), zt = zpow(alpha, w, static_cast<double>(tck::kTile));
-    P.z1024[p] = make_double2(z1.real(), z1.imag());
-    P.zT[p] = make_double2(zt.real(), zt.imag());
+    const cd zt = zpow(alpha, w, static_cast<double>(tck::kTile));
+    const double d2[2] = {zt.real(), zt.imag()};
+    std::memcpy(&img[tck::kZd + p * 16], d2, 16);
   }
-  for (size_t i = 0; i < img.size(); i += 4) {
-    float f;
-    std::memcpy(&f, &img[i], 4);
-    if (!std::isfinite(f)) fail(SFTGPU_EINVAL, "attenuation alpha*K too large for the requested precision");
-  }
-  cuda_check(cudaMalloc(&pl->d_tc_image, img.size()), "cudaMalloc tc image");
-  cuda_check(cudaMemcpy(pl->d_tc_image, img.data(), img.size(), cudaMemcpyHostToDevice), "copy tc image");
   // geometry: items = (signal, chunk); one persistent CTA per SM walks items in order
   const long long kSms = sftk::sm_count();
   const long long tiles_sig = (pl->count + tck::kTile - 1) / tck::kTile;
@@ -649,13 +645,37 @@ bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
         const cd z = zpow(alpha, ords[p].omega, 1.0), zE = zpow(alpha, ords[p].omega, static_cast<double>(E));
         g = std::abs(1.0 - z) < 1e-12 ? cd(static_cast<double>(E), 0.0) : (1.0 - zE) / (1.0 - z);
       }
-      P.g0[p] = make_double2(g.real(), g.imag());
+      const double g2[2] = {g.real(), g.imag()};
+      std::memcpy(&img[tck::kZd + (2 * tck::kMaxOrd + p) * 16], g2, 16);
     }
   }
+  // every table must be finite in its own precision (fp32 operands and scan constants,
+  // fp64 carry tables)
+  auto finite = [&](size_t a, size_t e, bool dbl) {
+    for (size_t i = a; i < e; i += dbl ? 8 : 4) {
+      double v;
+      if (dbl) {
+        std::memcpy(&v, &img[i], 8);
+      } else {
+        float f;
+        std::memcpy(&f, &img[i], 4);
+        v = f;
+      }
+      if (!std::isfinite(v)) return false;
+    }
+    return true;
+  };
+  if (!finite(0, tck::kZd, false) ||
+      !finite(tck::kZd, tck::kImage, true))
+    fail(SFTGPU_EINVAL, "attenuation alpha*K too large for the requested precision");
+  cuda_check(cudaMalloc(&pl->d_tc_image, img.size()), "cudaMalloc tc image");
+  cuda_check(cudaMemcpy(pl->d_tc_image, img.data(), img.size(), cudaMemcpyHostToDevice), "copy tc image");
   P.n = pl->n;
   P.lo = pl->lo;
   P.count = pl->count;
   P.K = K;
+  P.rl = static_cast<int>(((pl->lo + K) % 4 + 4) % 4);
+  P.rt = static_cast<int>(((pl->lo - K) % 4 + 4) % 4);
   P.boundary = pl->boundary;
   P.nord = nord;
   P.cplx = cplx ? 1 : 0;
@@ -950,6 +970,30 @@ bool make_out_map(sftgpu_plan* pl, void* out, long long ld_out, long long nsig, 
   return r == CUDA_SUCCESS;
 }
 
+// TMA view of the input for K4's loader: [signal][row][64 samples] with rows 32 samples
+// (128 B) apart, i.e. overlapping rows, so a box of 32 samples x 129 rows may start at
+// any 16-byte aligned sample. Needs a 16-byte aligned base and signal stride; rows are
+// limited so that every element of the view lies inside the signal.
+bool make_in_map(sftgpu_plan* pl, const void* x, long long ld_x, long long nsig, CUtensorMap* map,
+                 long long* rows_out) {
+  *rows_out = 0;
+  if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || (static_cast<unsigned long long>(ld_x) * sizeof(float)) % 16 != 0)
+    return false;
+  if (pl->n < 64 + 32) return false;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  const long long rows = (pl->n - 64) / 32 + 1;
+  const cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(nsig)};
+  const cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(ld_x) * sizeof(float)};
+  const cuuint32_t box[3] = {32, tck::kBoxRows, 1}, es[3] = {1, 1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(x), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  *rows_out = rows;
+  return true;
+}
+
 long long* g_tc_trace = nullptr;    // diagnostics: sftgpu_debug_set_tc_trace
 long long* g_scan_trace = nullptr;  // diagnostics: sftgpu_debug_set_scan_trace
 
@@ -965,11 +1009,17 @@ void run_tc(sftgpu_plan* pl, const void* x, long long ld_x, void* out, long long
       pl->tc_map_out = out;
       pl->tc_map_ld = ld_out;
     }
+    if (pl->tc_map_in != x || pl->tc_map_in_ld != ld_x) {
+      C.use_tma_in = make_in_map(pl, x, ld_x, pl->batch, &C.in_map, &C.in_rows) ? 1 : 0;
+      pl->tc_map_in = x;
+      pl->tc_map_in_ld = ld_x;
+    }
     P = C;
   } else {
     P = C;
     P.n_items = nsig * C.n_chunks;
     P.use_tma = make_out_map(pl, out, ld_out, nsig, &P.out_map) ? 1 : 0;
+    P.use_tma_in = make_in_map(pl, x, ld_x, nsig, &P.in_map, &P.in_rows) ? 1 : 0;
   }
   P.x = static_cast<const float*>(x);
   P.out = static_cast<float*>(out);
@@ -978,7 +1028,13 @@ void run_tc(sftgpu_plan* pl, const void* x, long long ld_x, void* out, long long
   const size_t rowb = static_cast<size_t>(ld_out) * sizeof(float) * (P.cplx ? 2 : 1);
   P.vec_ok = (reinterpret_cast<uintptr_t>(out) % 16 == 0 && rowb % 16 == 0) ? 1 : 0;
   if (const char* e = std::getenv("SFTGPU_TC_NO_TMA")) P.use_tma = e[0] == '1' ? 0 : P.use_tma;
+  if (const char* e = std::getenv("SFTGPU_TC_NO_TMA_IN")) P.use_tma_in = e[0] == '1' ? 0 : P.use_tma_in;
   P.trace = g_tc_trace;
+  if (const char* e = std::getenv("SFTGPU_TC_DBG")) P.dbg = std::atoi(e);
+  if (std::getenv("SFTGPU_TC_DEBUG"))
+    std::fprintf(stderr, "K4: lo=%lld K=%d n=%lld count=%lld rl=%d rt=%d in_rows=%lld tma_in=%d tma_out=%d cplx=%d nord=%d items=%lld warm=%lld skip0=%d\n",
+                 P.lo, P.K, P.n, P.count, P.rl, P.rt, P.in_rows, P.use_tma_in, P.use_tma, P.cplx, P.nord, P.n_items,
+                 P.warm_tiles, P.skip0);
   const int grid = static_cast<int>(std::min<long long>(pl->tc_grid, P.n_items));
   cuda_check(tck::launch_tc(P, grid, st), "sft_tc_kernel launch");
 }

@@ -195,3 +195,29 @@ def test_tc_subbatched_host_execution(sft, O):
     oh = np.empty(tuple(ref.shape), dtype=np.float32)
     plan.execute_host(xh, oh)
     assert np.array_equal(oh, ref.cpu().numpy())
+
+
+@pytest.mark.parametrize("offset,pad", [(1, 3), (0, 5), (2, 0)])
+def test_tc_unaligned_input(sft, O, offset, pad):
+    """Input rows that are not 16-byte aligned (base offset, odd leading dimension): K4's
+    loader cannot use TMA boxes or 16-byte copies and stages every stream per sample
+    (csrc/sft_tc.cuh, kMixed); results must match the aligned run bit for bit."""
+    import torch
+
+    spec = sft.make_transform_spec("MMS5P3", 600.0, 10.0, sft.TransformOptions(precision=0))
+    n, batch = 30000, 3
+    xb = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 21, batch, sft.Precision.Single)
+    plan = sft.TransformPlan(spec, n, batch, mode="tc")
+    ref = plan.empty_output()
+    plan.execute(xb, ref)
+    ld = n + pad
+    buf = torch.zeros(offset + batch * ld, dtype=torch.float32, device="cuda")
+    view = buf[offset:offset + batch * ld].view(batch, ld)
+    view[:, :n] = xb
+    out = plan.empty_output()
+    plan.execute(buf[offset:], out, ld_x=ld)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    xh = xb.double().cpu().numpy()
+    got = out.double().cpu().numpy()
+    assert rel_max(got[1, :, 0] + 1j * got[1, :, 1], oracle_transform(O, xh[1], 1, spec)) < 1e-5

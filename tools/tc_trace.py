@@ -22,7 +22,7 @@ torch.cuda.synchronize()
 lib.sftgpu_debug_set_tc_trace(None)
 t = tr.cpu().numpy().reshape(64, 16).astype(np.int64)
 t0 = t[t > 0].min()
-names = ["ld_issue", "xfull", "g1_iss", "scan_g1", "ss_rdy", "g2_iss", "epi_g2", "epi_end", "s_ld", "s_ks", "m_go", "L_wait", "L_iss0", "g2_go", "e_rel", "L_iss1"]
+names = ["ld_go", "mma_go", "g1_iss", "scan_g1", "st_tmem", "g2_iss", "epi_g2", "epi_end", "ph1", "ph2", "ld_full", "iss_done", "lead_rd", "tma_iss", "e_rel", "rd_start"]
 print("tile " + " ".join(f"{n:>8s}" for n in names))
 for g in range(64):
     print(f"{g:4d} " + " ".join(f"{(v - t0) if v > 0 else -1:8d}" for v in t[g]))
