@@ -51,7 +51,7 @@ namespace tck {
 
 struct Misc {
   uint64_t xfull[2], xfree[2], g1done[2], dfree[2], sready[2], g2done[2];
-  uint64_t full[kLoadAhead + 1];  // loader ring slot: TMA boxes landed
+  uint64_t fullL[kLoadAhead + 1], fullT[kLoadAhead + 1];  // loader ring slots landed (lead, trail)
   uint32_t tmem;
   double2 cy[2][kMaxOrd];  // tile carry (state entering the tile), fp64, by tile parity
 };
@@ -260,7 +260,7 @@ __device__ __noinline__ void store_masked(float* dst, float4 val, long long pos,
     if (pos + j / cw < cnt) dst[j] = e[j];
 }
 
-// named barriers: epilogue (3), loader (4), scan warps (5)
+// named barriers: epilogue (3), lead loaders (4), scan warps (5), trail loaders (6)
 __device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __device__ __forceinline__ float2 cmla(float2 z, float2 t, float2 a) {  // a + z t
@@ -308,14 +308,17 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
   }
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
-      umma::mbar_init(&M.xfull[b], 128);
+      umma::mbar_init(&M.xfull[b], 256);  // both stream groups
       umma::mbar_init(&M.xfree[b], 1);
       umma::mbar_init(&M.g1done[b], 1);
       umma::mbar_init(&M.dfree[b], 128);
       umma::mbar_init(&M.sready[b], 256);
       umma::mbar_init(&M.g2done[b], 1);
     }
-    for (int k = 0; k <= kLoadAhead; ++k) umma::mbar_init(&M.full[k], 129);  // TMA issuer + 128 cp.async arrivals
+    for (int k = 0; k <= kLoadAhead; ++k) {
+      umma::mbar_init(&M.fullL[k], 129);  // TMA issuer + 128 cp.async arrivals
+      umma::mbar_init(&M.fullT[k], 128);
+    }
     umma::mbar_fence_init();
   }
   __syncthreads();  // image (g0) in shared memory
@@ -328,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
   const uint32_t tmem = __shfl_sync(0xffffffffu, M.tmem, 0);  // warp-uniform
   constexpr int nord = NORD;
 
-  if (warp == 16) {
+  if (warp == 20) {
     // ================= MMA issuer: merged GEMM of tile gt, then the chunk-state GEMM of
     // the previous output tile (issued after it so that it overlaps that tile's scan)
     const uint64_t dbase = umma::desc_sw128(umma::smem_u32(sm));
@@ -406,51 +409,51 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     }
     if (pend >= 0) state_gemm();
   } else if (warp >= 12) {
-    // ================= loader: thread t = chunk row t = TMEM lane t (warp q: lanes [32 q, +32))
-    const int q = warp - 12, t = tid - 384;
-    const uint32_t lrow = static_cast<uint32_t>(q * 32) << 16;
-    unsigned char* const leads = sm + kLStage;
-    unsigned char* const trails = sm + kTrail;
+    // ================= loader: two groups of four warps, one per stream (warps 12-15 the
+    // lead, 16-19 the trail); in each, thread t = chunk row t = TMEM lane t (warp w: lanes
+    // [32 (w % 4), +32)). Each group stages its stream kLoadAhead tiles ahead into its
+    // ring (the lead by TMA, the trail and boundary segments by cp.async), then moves its
+    // rows into the X operand in TMEM.
+    const bool lead = warp < 16;
+    const int t = tid - (lead ? 384 : 512);
+    const uint32_t lrow = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const int bar_id = lead ? 4 : 6;
+    unsigned char* const ring = sm + (lead ? kLStage : kTrail);
+    const uint32_t stride = lead ? kLeadBytes : kTrailBytes;
+    uint64_t* const full = lead ? M.fullL : M.fullT;
     unsigned long long keep;  // lead lines are read again 2K positions later as the trail
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
     if (P.dbg & 2) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(keep));
-    // stream starts of a tile: lead x[n + K], trail x[n - K] from n = lo + o0, each
-    // rounded down to 16 bytes (rl / rt samples before the first one used)
-    auto starts = [&](const Walk& w, long long& al, long long& at, long long& jmin) {
+    // this group's stream of a tile: x[n + K] (lead) or x[n - K] (trail) from n = lo + o0,
+    // its start rounded down to 16 bytes (r samples before the first one used), its kind
+    const int r = lead ? P.rl : P.rt;
+    auto stream = [&](const Walk& w, long long& a, long long& jmin) {
       const long long lo = P.lo + w.obase, o0 = w.o0(P);
       jmin = lo - P.K;
-      al = lo + o0 + P.K - P.rl;
-      at = lo + o0 - P.K - P.rt;
+      a = lo + o0 + (lead ? P.K : -P.K) - r;
+      if (!lead && w.warm(P)) return static_cast<int>(kZero);  // warm tiles: no trail operand
+      return stream_kind(P, a, a + r, jmin, lead);
     };
-    // stage tile w into ring slot `slot`: the lead box by TMA (one thread, transaction
-    // bytes on full[slot]), everything else by cp.async from all 128 loader threads; every
-    // loader thread then arrives on full[slot] once its copies have landed (129 arrivals)
-    auto kinds = [&](const Walk& w, long long al, long long at, long long jmin, int& kl, int& kt) {
-      kl = stream_kind(P, al, al + P.rl, jmin, true);
-      kt = w.warm(P) ? kZero : stream_kind(P, at, at + P.rt, jmin, false);
-    };
+    // stage tile w into ring slot `slot`: a lead box by TMA (one thread, transaction bytes
+    // on fullL[slot]), everything else by cp.async from the group's 128 threads, each of
+    // which then arrives on the slot's barrier once its copies have landed
     auto issue = [&](const Walk& w, int slot, long long gtrace) {
       if (!w.valid) return;
-      long long al, at, jmin;
-      starts(w, al, at, jmin);
-      int kl, kt;
-      kinds(w, al, at, jmin, kl, kt);
-      unsigned char* const sl = leads + slot * kLeadBytes;
-      unsigned char* const st = trails + slot * kTrailBytes;
-      if (t == 0) {
+      long long a, jmin;
+      const int k = stream(w, a, jmin);
+      unsigned char* const sl = ring + slot * stride;
+      if (lead && t == 0) {
         trace_ev(P, gtrace, 13);
-        umma::mbar_arrive_tx(&M.full[slot], kl == kTma ? kBoxBytes : 0u);
-        if (kl == kTma)
-          umma::tma_load_3d(umma::smem_u32(sl), &P.in_map, &M.full[slot], static_cast<int>(al & 31),
-                            static_cast<int>(al >> 5), static_cast<int>(w.sig), keep);
+        umma::mbar_arrive_tx(&full[slot], k == kTma ? kBoxBytes : 0u);
+        if (k == kTma)
+          umma::tma_load_3d(umma::smem_u32(sl), &P.in_map, &full[slot], static_cast<int>(a & 31),
+                            static_cast<int>(a >> 5), static_cast<int>(w.sig), keep);
       }
-      const float* xs = P.x + w.sig * P.ld_x;
-      if (kl != kTma) stage_stream(P, xs, al, jmin, kl, t, sl);
-      stage_stream(P, xs, at, jmin, kt, t, st);
-      cp_async_arrive(&M.full[slot]);
+      if (k != kTma) stage_stream(P, P.x + w.sig * P.ld_x, a, jmin, k, t, sl);
+      cp_async_arrive(&full[slot]);
     };
-    // staging ring of kLoadAhead + 1 tiles: tile gt + kLoadAhead is issued before tile gt
-    // is moved into TMEM (its slot was last read by tile gt - 1, before its bar 4)
+    // ring of kLoadAhead + 1 tiles: tile gt + kLoadAhead is issued before tile gt is moved
+    // into TMEM (its slot was last read by tile gt - 1, before the group's barrier)
     uint32_t fph = 0;  // full[] phase bits
     Walk wi, w;
     wi.begin(P);
@@ -462,50 +465,34 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     for (long long gt = 0; w.valid; ++gt) {
       issue(wi, static_cast<int>((gt + kLoadAhead) % (kLoadAhead + 1)), gt + kLoadAhead);
       if (wi.valid) wi.advance(P);
-      if (t == 0) trace_ev(P, gt, 11);
+      if (lead && t == 0) trace_ev(P, gt, 11);
       const int slot = static_cast<int>(gt % (kLoadAhead + 1));
-      const bool warm = w.warm(P);
-      int kl, kt;
-      long long al, at, jmin;
-      starts(w, al, at, jmin);
-      kinds(w, al, at, jmin, kl, kt);
-      umma::mbar_wait(&M.full[slot], (fph >> slot) & 1u);
+      long long a, jmin;
+      const int k = stream(w, a, jmin);
+      umma::mbar_wait(&full[slot], (fph >> slot) & 1u);
       fph ^= 1u << slot;
       umma::fence_proxy_async();  // the cp.async writes precede a later TMA box in this slot
-      if (t == 0) trace_ev(P, gt, 10);
+      if (lead && t == 0) trace_ev(P, gt, 10);
       const int b = static_cast<int>(gt & 1);
       if (gt >= 2) umma::mbar_wait(&M.xfree[b], static_cast<uint32_t>(((gt >> 1) - 1) & 1));
       __syncwarp();
       umma::fence_after();
-      if (t == 0) trace_ev(P, gt, 0);
-      const unsigned char* sl = leads + slot * kLeadBytes;
-      const unsigned char* st = trails + slot * kTrailBytes;
-      const uint32_t tx = tmem + lrow + kTX + 128 * b;
-      // uniform streams: zero, x[0] (kFirst) or x[n - 1] (kLast)
-      auto uval = [&](const unsigned char* p, int k) {
-        return k == kZero ? 0.f : *reinterpret_cast<const float*>(p + kValOff + (k == kLast ? 4 : 0));
-      };
-      if (t == 0) trace_ev(P, gt, 15);
-      if (kl == kMixed || kt == kMixed) {
-        if (kl == kMixed) fill_mixed(P.n, P.boundary, umma::smem_u32(sl), t, al, jmin);
-        if (kt == kMixed) fill_mixed(P.n, P.boundary, umma::smem_u32(st), t, at, jmin);
-        bar_named(4, 128);
+      if (lead && t == 0) trace_ev(P, gt, 0);
+      const unsigned char* sl = ring + slot * stride;
+      const uint32_t tx = tmem + lrow + kTX + 128 * b + (lead ? 0 : 64);
+      if (k == kMixed) {
+        fill_mixed(P.n, P.boundary, umma::smem_u32(sl), t, a, jmin);
+        bar_named(bar_id, 128);
       }
-      if (kl == kTma || kl == kCp || kl == kMixed)
-        row_to_tmem(sl, P.rl, t, tx);
-      else
-        uniform_to_tmem(uval(sl, kl), tx);
-      if (t == 0) trace_ev(P, gt, 12);
-      if (!warm) {
-        if (kt == kTma || kt == kCp || kt == kMixed)
-          row_to_tmem(st, P.rt, t, tx + 64);
-        else
-          uniform_to_tmem(uval(st, kt), tx + 64);
-      }
+      if (k == kTma || k == kCp || k == kMixed)
+        row_to_tmem(sl, r, t, tx);
+      else if (lead || !w.warm(P))  // uniform: zero, x[0] (kFirst) or x[n - 1] (kLast)
+        uniform_to_tmem(k == kZero ? 0.f : *reinterpret_cast<const float*>(sl + kValOff + (k == kLast ? 4 : 0)), tx);
+      if (lead && t == 0) trace_ev(P, gt, 12);
       umma::tmem_wait_st();
       umma::fence_before();
       umma::mbar_arrive(&M.xfull[b]);
-      bar_named(4, 128);  // every row of the slot has been read: it may be refilled
+      bar_named(bar_id, 128);  // every row of the slot has been read: it may be refilled
       w.advance(P);
     }
   } else if (warp >= 8) {

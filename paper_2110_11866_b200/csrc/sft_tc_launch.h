@@ -13,7 +13,7 @@ constexpr int kQ = 32;           // positions per chunk (GEMM K per stream)
 constexpr int kNC = 128;         // chunks per tile (GEMM M)
 constexpr int kTile = kQ * kNC;  // 4096 positions
 constexpr int kMaxOrd = 8;       // 2 * orders <= 16 aggregate columns
-constexpr int kThreads = 544;    // 17 warps: scan (8), epilogue (4), loader (4), MMA issuer (1)
+constexpr int kThreads = 672;    // 21 warps: scan (8), epilogue (4), loaders (4 lead + 4 trail), MMA issuer
 
 // shared-memory image (bytes; SW128 K-major B operands, 1024-aligned regions).
 // BL/BT: [output rows (NO = 64 complex / 32 real) ; 16 aggregate rows] x 32 positions for
