@@ -52,47 +52,99 @@ namespace tck {
 struct Misc {
   uint64_t xfull[2], xfree[2], g1done[2], dfree[2], sready[2], g2done[2];
   uint64_t fullL[kLoadAhead + 1], fullT[kLoadAhead + 1];  // loader ring slots landed (lead, trail)
+  uint64_t drain, scandone, imgbar;  // scale switch: MMAs done, scans done, new image landed
   uint32_t tmem;
   double2 cy[2][kMaxOrd];  // tile carry (state entering the tile), fp64, by tile parity
 };
 static_assert(sizeof(Misc) <= 512, "Misc region");
 
-// (item, tile) walk shared by every role
+// Work of one CTA: a contiguous range [c, cend) of the global chunk sequence. Units
+// u = scale * nsig + sig are cut into fixed chunks (TcGeom); chunks are ordered scale-major
+// and partitioned over the CTAs by cost (warm-up + output tiles), so a CTA meets few
+// scales. A chunk (segment) is its warm-up tiles (from its own warm start, 2K positions
+// before its first output; leading constant ones of a unit's first chunk skipped)
+// followed by its output tiles.
+__device__ __forceinline__ int scale_of_chunk(const TcParams& P, int c) {
+  int lo = 0, hi = P.n_scales - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.geo[mid].cbase <= c) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+// tiles of all chunks before chunk c
+__device__ __forceinline__ int chunk_prefix(const TcParams& P, int c) {
+  if (c >= P.total_chunks) return P.total_cost;
+  const int s = scale_of_chunk(P, c);
+  const TcGeom& G = P.geo[s];
+  const int rem = c - G.cbase, u = rem / G.nc, k = rem - u * G.nc;
+  const int unit_cost = P.tiles_unit + G.nc * G.warm - G.skip0;
+  return G.wbase + u * unit_cost + k * (G.L + G.warm) - (k > 0 ? G.skip0 : 0);
+}
+// first chunk of CTA j: the smallest c with chunk_prefix(c) >= j * total_cost / grid
+__device__ __forceinline__ int cta_first_chunk(const TcParams& P, int j) {
+  const int target = static_cast<int>((static_cast<long long>(j) * P.total_cost) / gridDim.x);
+  int lo = 0, hi = P.total_chunks;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (chunk_prefix(P, mid) >= target) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
 struct Walk {
-  long long item, t, ntiles, obase, cnt, sig;
+  int c, cend;       // current chunk; range end
+  int sig, scale;
+  int l0, nout;      // first output tile of the chunk within its unit; output tiles
+  int W, t;          // warm-up tiles of the chunk's scale; tile cursor
   bool valid;
   __device__ void setup(const TcParams& P) {
-    valid = item < P.n_items;
+    valid = c < cend;
     if (!valid) return;
-    sig = item / P.n_chunks;
-    const long long ch = item - sig * P.n_chunks;
-    obase = ch * P.chunk_len;
-    cnt = P.count - obase < P.chunk_len ? P.count - obase : P.chunk_len;
-    ntiles = P.warm_tiles + (cnt + kTile - 1) / kTile;
-    t = ch == 0 ? P.skip0 : 0;  // skipped constant warm-up tiles (carry in closed form)
+    scale = scale_of_chunk(P, c);
+    const TcGeom& G = P.geo[scale];
+    const int rem = c - G.cbase, u = rem / G.nc, k = rem - u * G.nc;
+    sig = u;
+    l0 = k * G.L;
+    const int room = P.tiles_unit - l0;
+    nout = G.L < room ? G.L : room;
+    W = G.warm;
+    t = l0 == 0 ? G.skip0 : 0;  // skipped constant warm-up tiles
   }
   __device__ void begin(const TcParams& P) {
-    item = blockIdx.x;
+    c = cta_first_chunk(P, blockIdx.x);
+    cend = cta_first_chunk(P, blockIdx.x + 1);
     setup(P);
   }
   __device__ void advance(const TcParams& P) {
-    if (++t < ntiles) return;
-    item += gridDim.x;
+    if (++t < W + nout) return;
+    ++c;
     setup(P);
   }
-  __device__ bool warm(const TcParams& P) const { return t < P.warm_tiles; }
-  __device__ long long o0(const TcParams& P) const { return (t - P.warm_tiles) * kTile; }
-  __device__ bool last(const TcParams& P) const { return t + 1 == ntiles; }
+  __device__ int unit(const TcParams& P) const { return scale * P.nsig + sig; }
+  __device__ bool warm(const TcParams&) const { return t < W; }
+  __device__ long long obase() const { return static_cast<long long>(l0) * kTile; }
+  __device__ long long o0(const TcParams&) const { return static_cast<long long>(t - W) * kTile; }
+  __device__ long long cnt(const TcParams& P) const {
+    const long long cc = P.count - obase(), e = static_cast<long long>(nout) * kTile;
+    return cc < e ? cc : e;
+  }
+  __device__ bool last(const TcParams&) const { return t + 1 == W + nout; }
 };
 
-// fp64 state entering the first processed tile of `item` for order p: the closed-form
+// fp64 state entering the first processed tile of segment w for order p: the closed-form
 // contribution of the skipped constant warm-up tiles (0 when none are skipped)
-__device__ __forceinline__ double2 item_carry(const TcParams& P, const unsigned char* sm, long long item, int p) {
-  if (item >= P.n_items || P.skip0 == 0 || P.boundary == 0) return make_double2(0.0, 0.0);
-  const long long sig = item / P.n_chunks;
-  if (item - sig * P.n_chunks != 0) return make_double2(0.0, 0.0);
-  const double v = static_cast<double>(__ldg(P.x + sig * P.ld_x));
-  const double2 g0 = reinterpret_cast<const double2*>(sm + kZd)[2 * kMaxOrd + p];
+__device__ __forceinline__ const unsigned char* scale_image(const TcParams& P, int s) {
+  return reinterpret_cast<const unsigned char*>(
+      __ldg(reinterpret_cast<const unsigned long long*>(&P.scales[s].image)));
+}
+
+__device__ __forceinline__ double2 seg_carry(const TcParams& P, const Walk& w, int p) {
+  if (!w.valid || w.l0 != 0 || P.boundary == 0) return make_double2(0.0, 0.0);
+  if (P.geo[w.scale].skip0 == 0) return make_double2(0.0, 0.0);
+  const TcScale* S = P.scales + w.scale;
+  const double v = static_cast<double>(__ldg(P.x + w.sig * P.ld_x));
+  const double2 g0 = __ldg(&S->g0[p]);
   return make_double2(v * g0.x, v * g0.y);
 }
 
@@ -198,26 +250,26 @@ __device__ __forceinline__ void uniform_to_tmem(float v, uint32_t taddr) {
 template <int R>
 __device__ __forceinline__ void row_to_tmem_r(const unsigned char* slot, int c, uint32_t taddr) {
 #pragma unroll
-  for (int hh = 0; hh < 2; ++hh) {
-    float f[20];
+  for (int qq = 0; qq < 4; ++qq) {  // quarters of 8 columns keep the live registers low
+    float f[12];
 #pragma unroll
-    for (int k = 0; k < (R ? 5 : 4); ++k) {
-      const int p = 4 * hh + k, row = c + (p >> 3), pc = p & 7;
+    for (int k = 0; k < (R ? 3 : 2); ++k) {
+      const int p = 2 * qq + k, row = c + (p >> 3), pc = p & 7;
       const float4 v = *reinterpret_cast<const float4*>(slot + row * 128 + ((pc ^ (row & 7)) << 4));
       f[4 * k] = v.x;
       f[4 * k + 1] = v.y;
       f[4 * k + 2] = v.z;
       f[4 * k + 3] = v.w;
     }
-    uint32_t h[16], l[16];
+    uint32_t h[8], l[8];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < 8; ++i) {
       const float v = f[R + i];
       h[i] = __float_as_uint(v);
       l[i] = __float_as_uint(tf32_lo(v));
     }
-    umma::tmem_st16(taddr + 16 * hh, h);
-    umma::tmem_st16(taddr + 32 + 16 * hh, l);
+    umma::tmem_st8(taddr + 8 * qq, h);
+    umma::tmem_st8(taddr + 32 + 8 * qq, l);
   }
 }
 __device__ __forceinline__ void row_to_tmem(const unsigned char* slot, int r, int c, uint32_t taddr) {
@@ -302,9 +354,13 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
   const int NO = P.cplx ? 2 * kQ : kQ;  // output columns of the accumulator
 
   // ---- setup: operand image, barriers, TMEM (512 columns)
+  Walk w0;  // this CTA's first segment: its scale's operand image is loaded first
+  w0.begin(P);
+  if (!w0.valid) return;
   {
     uint4* dst = reinterpret_cast<uint4*>(sm);
-    for (int i = tid; i < static_cast<int>(kImage / 16); i += kThreads) dst[i] = __ldg(P.image + i);
+    const uint4* src = reinterpret_cast<const uint4*>(scale_image(P, w0.scale));
+    for (int i = tid; i < static_cast<int>(kImage / 16); i += kThreads) dst[i] = __ldg(src + i);
   }
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
@@ -315,6 +371,9 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       umma::mbar_init(&M.sready[b], 256);
       umma::mbar_init(&M.g2done[b], 1);
     }
+    umma::mbar_init(&M.drain, 1);
+    umma::mbar_init(&M.scandone, 256);
+    umma::mbar_init(&M.imgbar, 1);
     for (int k = 0; k <= kLoadAhead; ++k) {
       umma::mbar_init(&M.fullL[k], 129);  // TMA issuer + 128 cp.async arrivals
       umma::mbar_init(&M.fullT[k], 128);
@@ -322,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     umma::mbar_fence_init();
   }
   __syncthreads();  // image (g0) in shared memory
-  if (tid < kMaxOrd) M.cy[0][tid] = item_carry(P, sm, blockIdx.x, tid);
+  if (tid < kMaxOrd) M.cy[0][tid] = seg_carry(P, w0, tid);
   if (warp == 0) umma::tmem_alloc(&M.tmem, 512);
   umma::fence_proxy_async();
   umma::fence_before();
@@ -356,9 +415,28 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     };
     Walk w;
     w.begin(P);
+    int cur = w.scale, sw = 0;  // scale whose operand image is in shared memory; switches
     for (long long gt = 0; w.valid; ++gt) {
       const int b = static_cast<int>(gt & 1);
       const bool warm = w.warm(P);
+      if (w.scale != cur) {
+        // scale switch: every MMA and every scan of the old scale must be done with the
+        // image before the new one is copied over it (at most a few per CTA)
+        if (pend >= 0) state_gemm();
+        umma::commit_elect(&M.drain);
+        umma::mbar_wait(&M.drain, static_cast<uint32_t>(sw & 1));
+        umma::mbar_wait(&M.scandone, static_cast<uint32_t>(sw & 1));
+        if (lane == 0) {
+          umma::mbar_arrive_tx(&M.imgbar, kImage);
+          const unsigned char* src = scale_image(P, w.scale);
+          for (uint32_t o = 0; o < kImage; o += 16384)
+            umma::bulk_g2s(umma::smem_u32(sm) + o, src + o, kImage - o < 16384 ? kImage - o : 16384, &M.imgbar);
+        }
+        __syncwarp();
+        umma::mbar_wait(&M.imgbar, static_cast<uint32_t>(sw & 1));
+        cur = w.scale;
+        ++sw;
+      }
       const uint32_t xph = static_cast<uint32_t>((gt >> 1) & 1), dph = static_cast<uint32_t>(((gt >> 1) - 1) & 1);
       if (pend >= 0) {
         // the previous output tile's state GEMM goes first if its states are ready before
@@ -382,9 +460,20 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       if (lane == 0) trace_ev(P, gt, 1);
       const uint32_t d = tmem + (b ? kTD1 : kTD0), x = tmem + kTX + 128 * b;
       if (!warm) {
+        // the pending state GEMM slots in between k-steps as soon as its states are ready
+        // (issue blocks on the tensor pipe's queue: a whole merged GEMM takes ~1000 cycles)
+        auto poll = [&]() {
+          if (pend >= 0 && umma::mbar_test(&M.sready[u & 1], static_cast<uint32_t>((u >> 1) & 1))) {
+            state_gemm();
+            if (lane == 0) trace_ev(P, gt - 1, 5);
+          }
+        };
         merged_k<0>(dbase, d, x, idm);
+        poll();
         merged_k<1>(dbase, d, x, idm);
+        poll();
         merged_k<2>(dbase, d, x, idm);
+        poll();
         merged_k<3>(dbase, d, x, idm);
       } else if (NO == 64) {
         warm_k<0, 64>(dbase, d + 64, x, ida);
@@ -426,11 +515,13 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     if (P.dbg & 2) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(keep));
     // this group's stream of a tile: x[n + K] (lead) or x[n - K] (trail) from n = lo + o0,
     // its start rounded down to 16 bytes (r samples before the first one used), its kind
-    const int r = lead ? P.rl : P.rt;
-    auto stream = [&](const Walk& w, long long& a, long long& jmin) {
-      const long long lo = P.lo + w.obase, o0 = w.o0(P);
-      jmin = lo - P.K;
-      a = lo + o0 + (lead ? P.K : -P.K) - r;
+    auto stream = [&](const Walk& w, long long& a, long long& jmin, int& r) {
+      const TcGeom& G = P.geo[w.scale];
+      const int K = G.K;
+      r = lead ? G.rl : G.rt;
+      const long long lo = G.lo + w.obase(), o0 = w.o0(P);
+      jmin = lo - K;
+      a = lo + o0 + (lead ? K : -K) - r;
       if (!lead && w.warm(P)) return static_cast<int>(kZero);  // warm tiles: no trail operand
       return stream_kind(P, a, a + r, jmin, lead);
     };
@@ -440,14 +531,15 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     auto issue = [&](const Walk& w, int slot, long long gtrace) {
       if (!w.valid) return;
       long long a, jmin;
-      const int k = stream(w, a, jmin);
+      int r;
+      const int k = stream(w, a, jmin, r);
       unsigned char* const sl = ring + slot * stride;
       if (lead && t == 0) {
         trace_ev(P, gtrace, 13);
         umma::mbar_arrive_tx(&full[slot], k == kTma ? kBoxBytes : 0u);
         if (k == kTma)
           umma::tma_load_3d(umma::smem_u32(sl), &P.in_map, &full[slot], static_cast<int>(a & 31),
-                            static_cast<int>(a >> 5), static_cast<int>(w.sig), keep);
+                            static_cast<int>(a >> 5), w.sig, keep);
       }
       if (k != kTma) stage_stream(P, P.x + w.sig * P.ld_x, a, jmin, k, t, sl);
       cp_async_arrive(&full[slot]);
@@ -468,7 +560,8 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       if (lead && t == 0) trace_ev(P, gt, 11);
       const int slot = static_cast<int>(gt % (kLoadAhead + 1));
       long long a, jmin;
-      const int k = stream(w, a, jmin);
+      int r;
+      const int k = stream(w, a, jmin, r);
       umma::mbar_wait(&full[slot], (fph >> slot) & 1u);
       fph ^= 1u << slot;
       umma::fence_proxy_async();  // the cp.async writes precede a later TMA box in this slot
@@ -532,13 +625,13 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       umma::mbar_arrive(&M.dfree[gt & 1]);
       if (c == 0) trace_ev(P, gt, 14);
       ++u;
-      const long long o0 = w.o0(P), cnt = w.cnt;
+      const long long o0 = w.o0(P), cnt = w.cnt(P);
       if (P.use_tma) {
         // one thread hands the tile to the TMA engine: 128 rows x 32 floats per half
         umma::fence_proxy_async();
         bar_named(3, 128);
         if (c == 0) {
-          const int row0 = static_cast<int>((w.obase + o0) / kQ), sg = static_cast<int>(w.sig);
+          const int row0 = static_cast<int>((w.obase() + o0) / kQ), sg = w.unit(P);
           unsigned long long spol;
           asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(spol));
           for (int h = 0; h < halves; ++h) {
@@ -567,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
         continue;
       }
       bar_named(3, 128);
-      float* const orow = P.out + (w.sig * P.ld_out + w.obase) * cw;
+      float* const orow = P.out + (static_cast<long long>(w.unit(P)) * P.ld_out + w.obase()) * cw;
       for (int h = 0; h < halves; ++h) {
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
@@ -611,8 +704,14 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     Walk w;
     w.begin(P);
     long long u = 0;
+    int cur = w.scale, nsw = 0;  // scale whose tables are in shared memory; switches
     for (long long gt = 0; w.valid; ++gt) {
       const int b = static_cast<int>(gt & 1);
+      if (w.scale != cur) {  // the MMA issuer has copied the new scale's image
+        umma::mbar_wait(&M.imgbar, static_cast<uint32_t>(nsw & 1));
+        cur = w.scale;
+        ++nsw;
+      }
       umma::mbar_wait(&M.g1done[b], static_cast<uint32_t>((gt >> 1) & 1));
       if (tid == 0) trace_ev(P, gt, 3);
       __syncwarp();
@@ -662,7 +761,9 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
         if (lane == 31) {
           // carry into the next tile (fp64): z^{4096} C + (tile total)
           const double2 zt = zd[p];
-          M.cy[b ^ 1][p] = w.last(P) ? item_carry(P, sm, w.item + gridDim.x, p)
+          Walk nx = w;
+          if (w.last(P)) nx.advance(P);
+          M.cy[b ^ 1][p] = w.last(P) ? seg_carry(P, nx, p)
                                      : make_double2(fma(zt.x, C.x, fma(-zt.y, C.y, static_cast<double>(g.x))),
                                                     fma(zt.x, C.y, fma(zt.y, C.x, static_cast<double>(g.y))));
         }
@@ -694,6 +795,11 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
         umma::mbar_arrive(&M.sready[s]);
         if (tid == 0) trace_ev(P, gt, 4);
         ++u;
+      }
+      if (w.last(P)) {
+        Walk nx = w;
+        nx.advance(P);
+        if (nx.valid && nx.scale != w.scale) umma::mbar_arrive(&M.scandone);  // done with this image
       }
       w.advance(P);
     }

@@ -48,6 +48,38 @@ static_assert(kSmemBytes <= 232448, "shared memory budget (227 KB)");
 // chunk states [2][S_h (16) | S_l (16)], accumulators [2][outputs | aggregates]
 constexpr uint32_t kTX = 0, kTSS = 256, kTD0 = 320, kTD1 = 416;
 
+// One scale (spec) of a K4 launch: its operand image and stream geometry. A launch walks
+// units u = scale * nsig + sig; plans over one spec have one scale.
+struct TcScale {
+  const uint4* image;  // kImage bytes (operands and scan tables of this spec)
+  long long lo;        // first output position of the plan (n0 shift applied)
+  int K;               // half-width
+  int rl, rt;          // (lo + K) mod 4, (lo - K) mod 4: sample offsets of the lead / trail
+                       // streams from their 16-byte aligned starts
+  int warm_tiles;      // ceil(2K / 4096)
+  // Leading warm-up tiles of a unit's first segment whose lead samples all lie in the
+  // uniform boundary region (before sample 0) are not processed: the state they build is
+  // v * g0[p], v = x[0] (clamp) or 0 (zero boundary), g0 = sum_{e < E} z^e (host, fp64).
+  int skip0;
+  int pad;
+  double2 g0[kMaxOrd];
+};
+
+// Per-scale stream geometry in the parameter block (uniform, constant-cached reads on the
+// loaders' per-tile path); the rest of a scale lives in TcScale.
+constexpr int kMaxScales = 128;  // scales per launch (larger sets launch in groups)
+struct TcGeom {
+  int lo;                             // first output position (n0 shift applied)
+  int K;                              // half-width
+  unsigned char rl, rt, warm, skip0;  // see TcScale
+  // Units of this scale are cut into nc fixed chunks of L output tiles (the last one
+  // shorter); the cut depends only on the spec and the output count, never on the batch
+  // or the GPU, so results are reproducible bit for bit across batchings and devices.
+  int nc, L;
+  int cbase;  // global index of the scale's first chunk
+  int wbase;  // tiles (warm-up + output) of all earlier scales' chunks
+};
+
 struct TcParams {
   CUtensorMap out_map;  // TMA view of the output (see run_tc); valid when use_tma
   // TMA view of the input for the loader: [signal][row][64 samples], rows 32 samples
@@ -57,19 +89,17 @@ struct TcParams {
   long long in_rows;  // rows of in_map (row r + 1 of a box must lie below in_rows)
   const float* x;
   float* out;
-  long long n, ld_x, ld_out;  // ld_out in outputs (complex outputs count once)
-  long long lo, count;        // first output position, outputs per signal
-  long long chunk_len, n_chunks, n_items, warm_tiles;
-  int K, boundary, nord, cplx, vec_ok, use_tma, use_tma_in;
-  int rl, rt;  // (lo + K) mod 4, (lo - K) mod 4: sample offsets of the lead / trail streams
-               // from their 16-byte aligned box starts (uniform over the plan)
-  const uint4* image;  // kImage bytes
-  long long* trace;    // optional: per-tile event clocks of CTA 0 ([64][8]), tools/tc_trace.py
-  // Leading warm-up tiles of a signal's first chunk whose lead samples all lie in the
-  // uniform boundary region (before sample 0) are not processed: the state they build is
-  // v * g0[p], v = x[0] (clamp) or 0 (zero boundary), g0 = sum_{e < E} z^e (host, fp64).
-  int skip0;  // g0 lives in the image (kZd)
-  int dbg;    // experiment switches (SFTGPU_TC_DBG): 2 no lead L2 hint, 4 evict-first output stores
+  long long n, ld_x, ld_out;  // ld_out in outputs (complex outputs count once); out row = unit
+  long long count;            // outputs per unit
+  int tiles_unit;             // output tiles per unit, ceil(count / 4096)
+  int total_chunks;           // chunks of all units
+  int total_cost;             // tiles (warm-up + output) of all chunks (< 2^31)
+  int nsig, n_scales;
+  const TcScale* scales;  // [n_scales], device memory
+  TcGeom geo[kMaxScales];
+  int boundary, nord, cplx, vec_ok, use_tma, use_tma_in;
+  long long* trace;  // optional: per-tile event clocks of CTA 0 ([64][16]), tools/tc_trace.py
+  int dbg;           // experiment switches (SFTGPU_TC_DBG): 2 no lead L2 hint, 4 evict-first output stores
 };
 
 cudaError_t launch_tc(const TcParams& p, int grid, cudaStream_t s);

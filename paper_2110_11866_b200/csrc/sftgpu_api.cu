@@ -135,9 +135,10 @@ struct sftgpu_plan {
   int device = 0;
   // K4 (tensor-core chunked transform): operand image + parameter block
   int tc = 0;
-  void* d_tc_image = nullptr;
+  void* d_tc_image = nullptr;            // [scales][kImage] operand images
+  tck::TcScale* d_tc_scales = nullptr;  // [scales] descriptors
   tck::TcParams tcp{};
-  int tc_grid = 0;
+  int tc_grid = 0, tc_warm = 0;
   const void* tc_map_out = nullptr;  // output buffer the cached TMA map describes
   long long tc_map_ld = -1;
   const void* tc_map_in = nullptr;  // input buffer the cached loader map describes
@@ -185,6 +186,7 @@ struct sftgpu_plan {
       cudaFree(sb_out[k]);
     }
     cudaFree(d_tc_image);
+    cudaFree(d_tc_scales);
     if (ev_lb) cudaEventDestroy(ev_lb);
     cudaFree(d_ctrl);
     cudaFree(d_flags);
@@ -508,7 +510,9 @@ float tf32_head(float f) {
   return f;
 }
 
-bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
+// K4 eligibility of one lowered spec: fp32, <= 8 orders sharing one injection constant
+// z^{2K} (group modes 0 and 3). Returns the injection constant through cinj.
+bool tc_eligible(const sftgpu_plan* pl, const Lowered& lw, bool force, cd* cinj_out) {
   auto no = [&](const char* why) {
     if (force) fail(SFTGPU_EINVAL, std::string("tensor-core mode unavailable: ") + why);
     return false;
@@ -519,20 +523,19 @@ bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
   cd cA(0, 0), cB(0, 0);
   int na = 0;
   const int gm = detect_groups(ords, lw.alpha, lw.K, &cA, &cB, &na);
-  cd cinj;
   if (gm == sftk::kGroupShared)
-    cinj = cA;
+    *cinj_out = cA;
   else if (gm == sftk::kGroupSplit && na == 0)
-    cinj = cB;
+    *cinj_out = cB;
   else
     return no("orders do not share one injection constant");
-  if (!force) {
-    // auto: K4 once the transform spans >= 4 tiles per SM (SFTGPU_NO_TC=1 keeps K1)
-    const char* env = std::getenv("SFTGPU_NO_TC");
-    if (env && env[0] == '1') return false;
-    const long long tiles = pl->batch * ((pl->count + tck::kTile - 1) / tck::kTile);
-    if (tiles < 4LL * sftk::sm_count()) return false;
-  }
+  return true;
+}
+
+// The SW128 operand image and scan tables of one spec (sft_tc.cuh), and its stream
+// geometry for a plan whose first output position is lo.
+void tc_build_scale(const Lowered& lw, cd cinj, long long lo, std::vector<unsigned char>& img, tck::TcScale& sc) {
+  const std::vector<Order>& ords = lw.orders;
   const bool cplx = lw.complex_out;
   const int nord = static_cast<int>(ords.size());
   const double alpha = lw.alpha, pref = lw.prefactor;
@@ -550,7 +553,7 @@ bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
     D += A * b + B * std::conj(b);
   }
   auto Kp = [&](int p, cd v) { return cd(kw[p][0] * v.real() + kw[p][1] * v.imag(), kw[p][2] * v.real() + kw[p][3] * v.imag()); };
-  std::vector<unsigned char> img(tck::kImage, 0);
+  img.assign(tck::kImage, 0);
   auto put = [&](uint32_t region, int row, int k, float v) { std::memcpy(&img[region + sw128(row, k)], &v, 4); };
   auto put_split = [&](uint32_t rh, uint32_t rl, int row, int k, double v) {
     const float h = tf32_head(static_cast<float>(v));
@@ -603,8 +606,6 @@ bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
       put_split(tck::kBTh, tck::kBTl, NO + 2 * p, m, zt.real());
       put_split(tck::kBTh, tck::kBTl, NO + 2 * p + 1, m, zt.imag());
     }
-  tck::TcParams& P = pl->tcp;
-  std::memset(&P, 0, sizeof(P));
   for (int p = 0; p < nord; ++p) {
     const double w = ords[p].omega;
     for (int t = 0; t < 32; ++t) {
@@ -621,32 +622,29 @@ bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
     const double d2[2] = {zt.real(), zt.imag()};
     std::memcpy(&img[tck::kZd + p * 16], d2, 16);
   }
-  // geometry: items = (signal, chunk); one persistent CTA per SM walks items in order
-  const long long kSms = sftk::sm_count();
-  const long long tiles_sig = (pl->count + tck::kTile - 1) / tck::kTile;
-  long long chunks = 1;
-  if (pl->batch < kSms) chunks = std::min(tiles_sig, (kSms + pl->batch - 1) / pl->batch);
-  const long long per = (tiles_sig + chunks - 1) / chunks;
-  P.chunk_len = per * tck::kTile;
-  P.n_chunks = (pl->count + P.chunk_len - 1) / P.chunk_len;
-  P.n_items = pl->batch * P.n_chunks;
-  P.warm_tiles = (2LL * K + tck::kTile - 1) / tck::kTile;
+  std::memset(&sc, 0, sizeof(sc));
+  sc.lo = lo;
+  sc.K = K;
+  sc.rl = static_cast<int>(((lo + K) % 4 + 4) % 4);
+  sc.rt = static_cast<int>(((lo - K) % 4 + 4) % 4);
+  sc.warm_tiles = static_cast<int>((2LL * K + tck::kTile - 1) / tck::kTile);
   {
-    // leading warm-up tiles of chunk 0 whose lead samples j = lo + o + K are all < 0: the
-    // zeros before the warm start (Z positions) then the boundary value v; state after
-    // them = v * sum_{e < E} z^e with E = 4096 skip - Z
-    const long long W = P.warm_tiles, jfirst = pl->lo + K - W * tck::kTile;
+    // leading warm-up tiles of a unit's first segment whose lead samples j = lo + o + K
+    // are all < 0: the zeros before the warm start (Z positions) then the boundary value
+    // v; state after them = v * sum_{e < E} z^e with E = 4096 skip - Z
+    const long long W = sc.warm_tiles, jfirst = lo + K - W * tck::kTile;
     const long long skip = jfirst < 0 ? std::min(W, (-jfirst) / tck::kTile) : 0;
     const long long Z = W * tck::kTile - 2LL * K, E = skip * tck::kTile - Z;
-    P.skip0 = static_cast<int>(skip);
+    sc.skip0 = static_cast<int>(skip);
     for (int p = 0; p < nord; ++p) {
       cd g(0.0, 0.0);
       if (E > 0) {
         const cd z = zpow(alpha, ords[p].omega, 1.0), zE = zpow(alpha, ords[p].omega, static_cast<double>(E));
         g = std::abs(1.0 - z) < 1e-12 ? cd(static_cast<double>(E), 0.0) : (1.0 - zE) / (1.0 - z);
       }
-      const double g2[2] = {g.real(), g.imag()};
-      std::memcpy(&img[tck::kZd + (2 * tck::kMaxOrd + p) * 16], g2, 16);
+      if (!std::isfinite(g.real()) || !std::isfinite(g.imag()))
+        fail(SFTGPU_EINVAL, "attenuation alpha*K too large for the requested precision");
+      sc.g0[p] = make_double2(g.real(), g.imag());
     }
   }
   // every table must be finite in its own precision (fp32 operands and scan constants,
@@ -665,23 +663,88 @@ bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
     }
     return true;
   };
-  if (!finite(0, tck::kZd, false) ||
-      !finite(tck::kZd, tck::kImage, true))
+  if (!finite(0, tck::kZd, false) || !finite(tck::kZd, tck::kImage, true))
     fail(SFTGPU_EINVAL, "attenuation alpha*K too large for the requested precision");
-  cuda_check(cudaMalloc(&pl->d_tc_image, img.size()), "cudaMalloc tc image");
-  cuda_check(cudaMemcpy(pl->d_tc_image, img.data(), img.size(), cudaMemcpyHostToDevice), "copy tc image");
+}
+
+// Fixed chunking of every scale's units and the global chunk / cost prefixes (TcGeom):
+// chunks of at most max(256, 16 W) output tiles (warm-up <= 1/16 of a long chunk); a unit
+// that short stays whole. Depends on the specs and the output count only.
+void tc_geometry(tck::TcParams& P, const std::vector<tck::TcScale>& scales) {
+  long long cbase = 0, wbase = 0;
+  for (size_t i = 0; i < scales.size(); ++i) {
+    const tck::TcScale& sc = scales[i];
+    if (sc.lo < INT32_MIN / 2 || sc.lo > INT32_MAX / 2 || sc.warm_tiles > 255)
+      fail(SFTGPU_EINVAL, "tensor-core plan geometry out of range");
+    const long long T = P.tiles_unit, cmax = std::max<long long>(256, 16LL * sc.warm_tiles);
+    const long long nc = (T + cmax - 1) / cmax, L = (T + nc - 1) / nc;
+    tck::TcGeom& G = P.geo[i];
+    G.lo = static_cast<int>(sc.lo);
+    G.K = sc.K;
+    G.rl = static_cast<unsigned char>(sc.rl);
+    G.rt = static_cast<unsigned char>(sc.rt);
+    G.warm = static_cast<unsigned char>(sc.warm_tiles);
+    G.skip0 = static_cast<unsigned char>(sc.skip0);
+    G.nc = static_cast<int>(nc);
+    G.L = static_cast<int>(L);
+    G.cbase = static_cast<int>(cbase);
+    G.wbase = static_cast<int>(wbase);
+    cbase += nc * P.nsig;
+    wbase += (T + nc * sc.warm_tiles - sc.skip0) * P.nsig;
+    if (cbase >= (1LL << 31) || wbase >= (1LL << 31)) fail(SFTGPU_EINVAL, "tensor-core plan too large");
+  }
+  P.total_chunks = static_cast<int>(cbase);
+  P.total_cost = static_cast<int>(wbase);
+}
+
+// Uploads the images and scale descriptors of a K4 plan and fixes its launch geometry:
+// units = signals x scales (scale-major), one persistent CTA per SM over contiguous,
+// balanced ranges of output tiles.
+void tc_finish(sftgpu_plan* pl, const std::vector<std::vector<unsigned char>>& imgs,
+               std::vector<tck::TcScale>& scales, long long nsig, int nord, bool cplx) {
+  const size_t ns = scales.size();
+  cuda_check(cudaMalloc(&pl->d_tc_image, ns * tck::kImage), "cudaMalloc tc images");
+  for (size_t i = 0; i < ns; ++i) {
+    cuda_check(cudaMemcpy(static_cast<unsigned char*>(pl->d_tc_image) + i * tck::kImage, imgs[i].data(), tck::kImage,
+                          cudaMemcpyHostToDevice),
+               "copy tc image");
+    scales[i].image = reinterpret_cast<const uint4*>(static_cast<unsigned char*>(pl->d_tc_image) + i * tck::kImage);
+  }
+  cuda_check(cudaMalloc(&pl->d_tc_scales, ns * sizeof(tck::TcScale)), "cudaMalloc tc scales");
+  cuda_check(cudaMemcpy(pl->d_tc_scales, scales.data(), ns * sizeof(tck::TcScale), cudaMemcpyHostToDevice),
+             "copy tc scales");
+  tck::TcParams& P = pl->tcp;
+  std::memset(&P, 0, sizeof(P));
   P.n = pl->n;
-  P.lo = pl->lo;
   P.count = pl->count;
-  P.K = K;
-  P.rl = static_cast<int>(((pl->lo + K) % 4 + 4) % 4);
-  P.rt = static_cast<int>(((pl->lo - K) % 4 + 4) % 4);
+  P.tiles_unit = static_cast<int>((pl->count + tck::kTile - 1) / tck::kTile);
+  P.nsig = static_cast<int>(nsig);
+  P.n_scales = static_cast<int>(ns);
+  P.scales = pl->d_tc_scales;
+  if (ns > static_cast<size_t>(tck::kMaxScales)) fail(SFTGPU_EINVAL, "too many scales for one tensor-core launch");
+  tc_geometry(P, scales);
   P.boundary = pl->boundary;
   P.nord = nord;
   P.cplx = cplx ? 1 : 0;
-  P.image = static_cast<const uint4*>(pl->d_tc_image);
-  pl->tc_grid = static_cast<int>(std::min(kSms, P.n_items));
+  pl->tc_warm = scales[0].warm_tiles;
+  pl->tc_grid = static_cast<int>(std::min<long long>(sftk::sm_count(), P.total_chunks));
   pl->tc = 1;
+}
+
+bool build_tc(sftgpu_plan* pl, const Lowered& lw, bool force) {
+  cd cinj;
+  if (!tc_eligible(pl, lw, force, &cinj)) return false;
+  if (!force) {
+    // auto: K4 once the transform spans >= 4 tiles per SM (SFTGPU_NO_TC=1 keeps K1)
+    const char* env = std::getenv("SFTGPU_NO_TC");
+    if (env && env[0] == '1') return false;
+    const long long tiles = pl->batch * ((pl->count + tck::kTile - 1) / tck::kTile);
+    if (tiles < 4LL * sftk::sm_count()) return false;
+  }
+  std::vector<std::vector<unsigned char>> imgs(1);
+  std::vector<tck::TcScale> scales(1);
+  tc_build_scale(lw, cinj, pl->lo, imgs[0], scales[0]);
+  tc_finish(pl, imgs, scales, pl->batch, static_cast<int>(lw.orders.size()), lw.complex_out);
   return true;
 }
 
@@ -1003,21 +1066,31 @@ void run_tc(sftgpu_plan* pl, const void* x, long long ld_x, void* out, long long
             long long nsig = -1) {
   tck::TcParams& C = pl->tcp;
   tck::TcParams P;
-  if (nsig < 0 || nsig == pl->batch) {
+  // output rows: units (signals x scales); input rows: signals
+  const long long rows = static_cast<long long>(C.nsig) * C.n_scales;
+  if (nsig < 0 || nsig == C.nsig) {
     if (pl->tc_map_out != out || pl->tc_map_ld != ld_out) {
-      C.use_tma = make_out_map(pl, out, ld_out, pl->batch, &C.out_map) ? 1 : 0;
+      C.use_tma = make_out_map(pl, out, ld_out, rows, &C.out_map) ? 1 : 0;
       pl->tc_map_out = out;
       pl->tc_map_ld = ld_out;
     }
     if (pl->tc_map_in != x || pl->tc_map_in_ld != ld_x) {
-      C.use_tma_in = make_in_map(pl, x, ld_x, pl->batch, &C.in_map, &C.in_rows) ? 1 : 0;
+      C.use_tma_in = make_in_map(pl, x, ld_x, C.nsig, &C.in_map, &C.in_rows) ? 1 : 0;
       pl->tc_map_in = x;
       pl->tc_map_in_ld = ld_x;
     }
     P = C;
-  } else {
+  } else {  // sub-batch of a single-scale plan
     P = C;
-    P.n_items = nsig * C.n_chunks;
+    P.nsig = static_cast<int>(nsig);
+    std::vector<tck::TcScale> one(1);
+    one[0].lo = P.geo[0].lo;
+    one[0].K = P.geo[0].K;
+    one[0].rl = P.geo[0].rl;
+    one[0].rt = P.geo[0].rt;
+    one[0].warm_tiles = P.geo[0].warm;
+    one[0].skip0 = P.geo[0].skip0;
+    tc_geometry(P, one);
     P.use_tma = make_out_map(pl, out, ld_out, nsig, &P.out_map) ? 1 : 0;
     P.use_tma_in = make_in_map(pl, x, ld_x, nsig, &P.in_map, &P.in_rows) ? 1 : 0;
   }
@@ -1031,11 +1104,7 @@ void run_tc(sftgpu_plan* pl, const void* x, long long ld_x, void* out, long long
   if (const char* e = std::getenv("SFTGPU_TC_NO_TMA_IN")) P.use_tma_in = e[0] == '1' ? 0 : P.use_tma_in;
   P.trace = g_tc_trace;
   if (const char* e = std::getenv("SFTGPU_TC_DBG")) P.dbg = std::atoi(e);
-  if (std::getenv("SFTGPU_TC_DEBUG"))
-    std::fprintf(stderr, "K4: lo=%lld K=%d n=%lld count=%lld rl=%d rt=%d in_rows=%lld tma_in=%d tma_out=%d cplx=%d nord=%d items=%lld warm=%lld skip0=%d\n",
-                 P.lo, P.K, P.n, P.count, P.rl, P.rt, P.in_rows, P.use_tma_in, P.use_tma, P.cplx, P.nord, P.n_items,
-                 P.warm_tiles, P.skip0);
-  const int grid = static_cast<int>(std::min<long long>(pl->tc_grid, P.n_items));
+  const int grid = static_cast<int>(std::min<long long>(pl->tc_grid, P.total_chunks));
   cuda_check(tck::launch_tc(P, grid, st), "sft_tc_kernel launch");
 }
 
@@ -1557,7 +1626,9 @@ int sftgpu_plan_describe(const sftgpu_plan* pl, int64_t* info, int n_info) {
     int64_t orders = 0;
     for (const Group& g : pl->groups) orders += g.nord;
     if (pl->tc) {
-      const int64_t v[11] = {0, 0, 0, tck::kTile, pl->tcp.warm_tiles, pl->tcp.n_chunks, pl->tc_grid, 1,
+      const long long units = static_cast<long long>(pl->tcp.nsig) * pl->tcp.n_scales;
+      const int64_t v[11] = {0, 0, 0, tck::kTile, pl->tc_warm, pl->tcp.total_chunks / std::max(1LL, units),
+                             pl->tc_grid, 1,
                              pl->tcp.nord, -1, 1};
       for (int i = 0; i < n_info && i < 11; ++i) info[i] = v[i];
       return;

@@ -99,14 +99,20 @@ def test_tc_skipped_constant_warmup(sft, O, boundary):
 
 
 def test_tc_ranged_plan_matches_full(sft, O):
-    """Output-range plans (chunk sharding with halo) reproduce the full transform."""
+    """Output-range plans (chunk sharding with halo) reproduce the full transform. The two
+    are different fp32 evaluations of the same sums (the range plan warms up from its own
+    window start), so they agree to fp32 rounding; each is checked against the fp64
+    oracle at the north_star bound."""
     spec = sft.make_transform_spec("MDS5P6", 2000.0, 10.0, sft.TransformOptions(precision=0))
     n = 60000
     xb = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 3, 1, sft.Precision.Single)
     _, full = _run(sft, spec, xb, "tc")
+    ref = oracle_transform(O, xb[0].double().cpu().numpy(), 1, spec)
+    assert rel_max(full[0], ref) < 1e-5
     for b, c in ((0, 7000), (23456, 20000), (n - 9999, 9999)):
         _, part = _run(sft, spec, xb, "tc", 1, (b, c))
-        assert rel_max(part[0], full[0, b:b + c]) < 2e-6
+        assert rel_max(part[0], full[0, b:b + c]) < 5e-6
+        assert rel_max(part[0], ref[b:b + c]) < 1e-5
 
 
 def test_tc_selection(sft, O):
@@ -167,14 +173,21 @@ def test_tc_long_signal_chunks_match_cuda_core(sft, O):
 
 
 def test_tc_batch_smaller_than_sms(sft, O):
-    """A few signals, each split into several chunk items (batch < 148)."""
+    """A few long signals, each cut into fixed chunks (at most max(256, 16 W) output tiles,
+    each with its own warm-up) spread over the persistent CTAs; the cut depends on the
+    spec and the length only, so every signal's result is bit-identical whether it runs
+    in a batch or alone."""
+    import torch
+
     spec = sft.make_transform_spec("MMS5P3", 1000.0, 10.0, sft.TransformOptions(precision=0))
-    n, B = 400000, 5
+    n, B = 1200000, 3
     xb = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 8, B, sft.Precision.Single)
     plan, tc = _run(sft, spec, xb, "tc")
-    assert plan.describe()["chunks_per_signal"] > 1
+    assert plan.describe()["chunks_per_signal"] == 2
     _, k1 = _run(sft, spec, xb, "seq")
     assert rel_max(tc, k1) < 1e-5
+    _, alone = _run(sft, spec, xb[1:2].contiguous(), "tc")
+    assert np.array_equal(alone[0], tc[1])
 
 
 def test_tc_subbatched_host_execution(sft, O):
