@@ -234,6 +234,17 @@ int sftgpu_transform_plan_create_range(const sftgpu_spec* spec, int64_t n, int64
  * transforms when they span >= 4 x 148 tiles of 4096 outputs (SFTGPU_NO_TC=1 disables). */
 int sftgpu_transform_plan_create_ex(const sftgpu_spec* spec, int64_t n, int64_t batch, int boundary,
                                     int64_t out_begin, int64_t out_count, int mode_hint, sftgpu_plan** plan);
+/* Multi-scale plan (scalogram, BASELINE config 5): n_specs transforms of ONE signal of n
+ * samples, output rows s = 0..n_specs-1 ([n_specs][ld_out] real or [n_specs][ld_out][2]
+ * complex), each over output range [out_begin, out_begin + out_count). One persistent
+ * tensor-core (K4) launch walks every scale's fixed chunks, balanced over the SMs by cost,
+ * instead of one launch per scale (replaces the reference's per-scale
+ * apply_transform / morlet_direct_transform calls, proj/src/transforms.cpp:337-371).
+ * Every spec must be fp32 and K4-eligible with the same number of orders and output kind
+ * (all Morlet-direct specs of a scalogram are); at most 128 specs per plan. Executed with
+ * sftgpu_transform_execute (x: the one signal) or sftgpu_transform_execute_host. */
+int sftgpu_multiscale_plan_create(const sftgpu_spec* specs, int n_specs, int64_t n, int boundary,
+                                  int64_t out_begin, int64_t out_count, sftgpu_plan** plan);
 int sftgpu_transform_execute(sftgpu_plan* plan, const void* x, int64_t ld_x, void* out,
                              int64_t ld_out, void* stream);
 /* Same, from/to HOST memory of the plan's precision (host<->device copies included;

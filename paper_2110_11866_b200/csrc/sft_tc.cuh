@@ -607,23 +607,28 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       __syncwarp();
       umma::fence_after();
       const uint32_t dcol = (gt & 1) ? kTD1 : kTD0;
-      // the previous tile's TMA stores must have read the staging area
-      if (c == 0 && P.use_tma) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      bar_named(3, 128);
-      // accumulator -> staging (row c: 8 chunks of 16 B per half, chunk q at q ^ (c & 7):
-      // the TMA SWIZZLE_128B layout of a [128 rows][32 floats] box)
-      for (int h = 0; h < halves; ++h) {
-        uint32_t v[32];
-        umma::tmem_ld32(tmem + lrow + dcol + 32 * h, v);
-        umma::tmem_wait_ld();
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<uint4*>(stgo + h * 16384 + c * 128 + ((q ^ (c & 7)) << 4)) =
-              make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-      }
+      // accumulator -> registers, then release it at once (it gates the merged GEMM two
+      // tiles on); then registers -> staging (row c: 8 chunks of 16 B per half, chunk q at
+      // q ^ (c & 7): the TMA SWIZZLE_128B layout of a [128 rows][32 floats] box)
+      uint32_t v[2][32];
+      umma::tmem_ld32(tmem + lrow + dcol, v[0]);
+      if (halves == 2) umma::tmem_ld32(tmem + lrow + dcol + 32, v[1]);
+      umma::tmem_wait_ld();
       umma::fence_before();
       umma::mbar_arrive(&M.dfree[gt & 1]);
       if (c == 0) trace_ev(P, gt, 14);
+      // the previous tile's TMA stores must have read the staging area
+      if (c == 0 && P.use_tma) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      bar_named(3, 128);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h < halves) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<uint4*>(stgo + h * 16384 + c * 128 + ((q ^ (c & 7)) << 4)) =
+                make_uint4(v[h][4 * q], v[h][4 * q + 1], v[h][4 * q + 2], v[h][4 * q + 3]);
+        }
+      }
       ++u;
       const long long o0 = w.o0(P), cnt = w.cnt(P);
       if (P.use_tma) {

@@ -106,6 +106,7 @@ struct sftgpu_plan {
   int mode = sftk::kModeReal;
   int conv = 0;  // GCT3/MCT3 direct convolution plan
   long long n = 0, batch = 0, lo = 0, count = 0;
+  long long in_batch = -1;  // input signals when not `batch` (multi-scale plans: 1 signal, batch = scales)
   int K = 1, boundary = SFTGPU_BOUNDARY_CLAMP;
   int L = 8, NT = 128;
   int seq = 0;  // 1: one CTA walks a whole (signal, chunk), no look-back workspace
@@ -1465,6 +1466,53 @@ int sftgpu_components_plan_create(const sftgpu_config* cfgs, int n_orders, int64
   });
 }
 
+int sftgpu_multiscale_plan_create(const sftgpu_spec* specs, int n_specs, int64_t n, int boundary,
+                                  int64_t out_begin, int64_t out_count, sftgpu_plan** plan) {
+  return guarded([&] {
+    if (!plan) fail(SFTGPU_EINVAL, "null plan pointer");
+    *plan = nullptr;
+    if (!specs || n_specs < 1 || n_specs > tck::kMaxScales) fail(SFTGPU_EINVAL, "need 1..128 specs");
+    if (n < 1) fail(SFTGPU_EINVAL, "Signal: need at least one sample");
+    if (boundary != SFTGPU_BOUNDARY_ZERO && boundary != SFTGPU_BOUNDARY_CLAMP)
+      fail(SFTGPU_EINVAL, "unknown boundary policy");
+    if (out_begin < 0 || out_count < 1 || out_begin + out_count > n) fail(SFTGPU_EINVAL, "output range outside the signal");
+    require_device();
+    auto pl = std::make_unique<sftgpu_plan>();
+    cuda_check(cudaGetDevice(&pl->device), "cudaGetDevice");
+    pl->precision = SFTGPU_SINGLE;
+    pl->n = n;
+    pl->batch = n_specs;
+    pl->in_batch = 1;
+    pl->boundary = boundary;
+    pl->count = out_count;
+    std::vector<std::vector<unsigned char>> imgs(n_specs);
+    std::vector<tck::TcScale> scales(n_specs);
+    int nord = -1;
+    bool cplx = false;
+    for (int i = 0; i < n_specs; ++i) {
+      const sftb::Spec s = spec_from_c(&specs[i]);
+      if (s.precision != SFTGPU_SINGLE) fail(SFTGPU_EINVAL, "multi-scale plans are single precision");
+      if (s.kind == sftb::TKind::TruncGauss || s.kind == sftb::TKind::TruncMorlet)
+        fail(SFTGPU_EINVAL, "multi-scale plans take sliding-transform specs");
+      const Lowered lw = lower_spec(s);
+      cd cinj;
+      tc_eligible(pl.get(), lw, true, &cinj);
+      if (i == 0) {
+        nord = static_cast<int>(lw.orders.size());
+        cplx = lw.complex_out;
+        pl->K = lw.K;
+        pl->lo = out_begin - static_cast<long long>(s.n0);
+        pl->mode = cplx ? sftk::kModeComplex : sftk::kModeReal;
+      } else if (static_cast<int>(lw.orders.size()) != nord || lw.complex_out != cplx) {
+        fail(SFTGPU_EINVAL, "multi-scale plan: every spec needs the same number of orders and output kind");
+      }
+      tc_build_scale(lw, cinj, out_begin - static_cast<long long>(s.n0), imgs[i], scales[i]);
+    }
+    tc_finish(pl.get(), imgs, scales, 1, nord, cplx);
+    *plan = pl.release();
+  });
+}
+
 int sftgpu_transform_execute(sftgpu_plan* pl, const void* x, int64_t ld_x, void* out, int64_t ld_out,
                              void* stream) {
   return guarded([&] {
@@ -1484,7 +1532,9 @@ int sftgpu_transform_execute(sftgpu_plan* pl, const void* x, int64_t ld_x, void*
 }
 
 namespace {
-size_t plan_in_bytes(const sftgpu_plan* pl) { return static_cast<size_t>(pl->n * pl->batch) * elem_size(pl->precision); }
+size_t plan_in_bytes(const sftgpu_plan* pl) {
+  return static_cast<size_t>(pl->n * (pl->in_batch >= 0 ? pl->in_batch : pl->batch)) * elem_size(pl->precision);
+}
 size_t plan_out_bytes(const sftgpu_plan* pl) {
   return static_cast<size_t>(pl->count * pl->batch) * elem_size(pl->precision) * (pl->mode == sftk::kModeComplex ? 2 : 1);
 }
@@ -1563,7 +1613,7 @@ int sftgpu_transform_execute_host(sftgpu_plan* pl, const void* x_host, void* out
     if (!pl || pl->is_components) fail(SFTGPU_EINVAL, "not a transform plan");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t xb = plan_in_bytes(pl), ob = plan_out_bytes(pl);
-    if (pl->tc && pl->batch >= 4 && xb + ob >= (256u << 20)) {
+    if (pl->tc && pl->in_batch < 0 && pl->batch >= 4 && xb + ob >= (256u << 20)) {
       execute_host_subbatched(pl, x_host, out_host, st);
       return;
     }

@@ -12,8 +12,8 @@ across ranks (one process per GPU) without any cross-GPU carry:
 
 Collectives: the input is broadcast once before any transform runs; the optional
 final gather to rank 0 is point-to-point (NCCL has no gather), timed separately.
-The per-scale kernel launches are the product K1 kernel (``TransformPlan``); the
-``executor`` hook exists so the distributed host logic can be exercised on CPU
+The kernels are the product ones: one persistent multi-scale K4 launch per <= 128 scales
+(``MultiScalePlan``), else per-scale ``TransformPlan``s; the ``executor`` hook exists so the distributed host logic can be exercised on CPU
 (gloo) with a checker in tests.
 """
 from __future__ import annotations
@@ -97,19 +97,31 @@ class Scalogram:
         self.plans = []
         self.n_streams = streams
         self._streams = None
+        self.multi = []  # (first row, MultiScalePlan over rows [first, first + plan.batch))
         if executor is None:
-            # mode "auto": K4 (tensor cores, one persistent CTA per SM per scale) where the
-            # scale qualifies, else sequential K1 plans (chunked, few CTAs each, so scales
-            # run concurrently on several streams with no inter-CTA look-back)
-            for i in self.rows:
-                p = S.TransformPlan(self.specs[i], n, 1, boundary, (self.begin, self.count), mode=mode)
-                if mode == "auto" and not p.describe()["tensor_cores"]:
-                    p = S.TransformPlan(self.specs[i], n, 1, boundary, (self.begin, self.count), mode="seq")
-                self.plans.append(p)
+            # mode "auto": the rank's scales in persistent multi-scale tensor-core launches
+            # (K4 over every scale's fixed chunks, <= 128 scales each) when every spec
+            # qualifies; otherwise one plan per scale: K4 where the scale qualifies, else
+            # sequential K1 plans (chunked, few CTAs each, so scales run concurrently on
+            # several streams with no inter-CTA look-back)
+            rng = (self.begin, self.count)
+            if mode == "auto":
+                try:
+                    for r0 in range(0, len(self.rows), 128):
+                        sub = [self.specs[i] for i in self.rows[r0:r0 + 128]]
+                        self.multi.append((r0, S.MultiScalePlan(sub, n, boundary, rng)))
+                except ValueError:
+                    self.multi = []
+            if not self.multi:
+                for i in self.rows:
+                    p = S.TransformPlan(self.specs[i], n, 1, boundary, rng, mode=mode)
+                    if mode == "auto" and not p.describe()["tensor_cores"]:
+                        p = S.TransformPlan(self.specs[i], n, 1, boundary, rng, mode="seq")
+                    self.plans.append(p)
 
     @property
     def launches(self) -> int:
-        return sum(p.launches for p in self.plans)
+        return sum(p.launches for p in self.plans) + sum(p.launches for _, p in self.multi)
 
     def output_bytes(self, itemsize: int = 4) -> int:
         return len(self.rows) * self.count * 2 * itemsize
@@ -127,6 +139,10 @@ class Scalogram:
             return out
         import torch
 
+        if self.multi:
+            for r0, p in self.multi:
+                p.execute(x, out[r0:r0 + p.batch])
+            return out
         cur = torch.cuda.current_stream()
         if self._streams is None:
             self._streams = [torch.cuda.Stream() for _ in range(self.n_streams)]

@@ -28,7 +28,7 @@ __all__ = [
     "effective_kernel", "components_over", "sft_components", "asft_components", "sft_via_sliding_sum",
     "truncated_convolution", "fit_gaussian_bundle", "fit_morlet_direct", "fit_morlet_envelope",
     "fit_mmse", "select_optimal_ps", "tune_beta_gauss", "gauss_kernel_rmse",
-    "morlet_direct_kernel_rmse", "morlet_multiply_kernel_rmse", "TransformPlan", "ComponentsPlan",
+    "morlet_direct_kernel_rmse", "morlet_multiply_kernel_rmse", "TransformPlan", "MultiScalePlan", "ComponentsPlan",
     "FitDegenerateError", "SftGpuError", "write_coefficient_sets", "read_coefficient_sets",
     "morlet_direct_spec_from_coeffs", "sliding_sum_plan", "sliding_sum_flat", "sliding_sum_blocked8",
 ]
@@ -697,6 +697,43 @@ class TransformPlan:
         if getattr(self, "_h", None) and getattr(self, "_destroy", None):
             self._destroy(self._h)
             self._h = None
+
+
+class MultiScalePlan(TransformPlan):
+    """All scales of a scalogram over ONE signal in one persistent tensor-core launch
+    (``sftgpu_multiscale_plan_create``): x is the signal ([n] or [1][n], fp32), out is
+    [len(specs)][count][2] (complex) or [len(specs)][count]. Every spec must be fp32,
+    K4-eligible, with the same order count and output kind (ValueError otherwise);
+    at most 128 specs."""
+
+    def __init__(self, specs, n: int, boundary=BoundaryPolicy.Clamp, out_range=None):
+        specs = list(specs)
+        arr = (_abi.Spec * len(specs))(*[sp._raw for sp in specs])
+        begin, count = out_range if out_range is not None else (0, n)
+        h = C.c_void_p()
+        check(lib().sftgpu_multiscale_plan_create(arr, len(specs), n, int(boundary), begin, count, C.byref(h)))
+        self._h = h
+        self._destroy = lib().sftgpu_plan_destroy
+        self.n, self.batch, self.out_begin, self.count = n, len(specs), begin, count
+        self.complex_out = bool(lib().sftgpu_plan_output_is_complex(h))
+        self.precision = Precision.Single
+        self.launches = lib().sftgpu_plan_launches_per_execute(h)
+        self.device = _torch().cuda.current_device()
+        self._cw = 2 if self.complex_out else 1
+
+    def execute(self, x, out, stream=None, ld_x=None, ld_out=None):
+        torch = _torch()
+        lo = ld_out or self.count
+        dt = self.dtype()
+        _check_device_buffer(x, dt, self.n, self.device, "x")
+        _check_device_buffer(out, dt, ((self.batch - 1) * lo + self.count) * self._cw, self.device, "out")
+        st = C.c_void_p(stream) if stream is not None else _stream_ptr(torch)
+        check(lib().sftgpu_transform_execute(self._h, C.c_void_p(x.data_ptr()), ld_x or self.n,
+                                             C.c_void_p(out.data_ptr()), lo, st))
+
+    def _check_host(self, x_host, out_host):
+        _check_host_buffer(x_host, 4, self.n, "x_host")
+        _check_host_buffer(out_host, 4, self.batch * self.count * self._cw, "out_host")
 
 
 def _run(sig: Signal, spec: TransformSpec) -> TransformResult:

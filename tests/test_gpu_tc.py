@@ -234,3 +234,45 @@ def test_tc_unaligned_input(sft, O, offset, pad):
     xh = xb.double().cpu().numpy()
     got = out.double().cpu().numpy()
     assert rel_max(got[1, :, 0] + 1j * got[1, :, 1], oracle_transform(O, xh[1], 1, spec)) < 1e-5
+
+
+@pytest.mark.parametrize("n,out_range", [(300000, None), (1 << 21, None), (1 << 21, (700001, 500000))])
+def test_multiscale_plan_matches_per_scale(sft, O, n, out_range):
+    """One persistent multi-scale K4 launch over several scales of one signal (config 5's
+    shape, sftgpu_multiscale_plan_create) equals the per-scale plans bit for bit (same
+    fixed chunking per spec; scale switches reload the operand image mid-CTA), and the
+    fp64 oracle on a window."""
+    import torch
+    from paper_2110_11866_b200 import scalogram as SG
+
+    sigmas = [16.0, 90.0, 700.0, 2500.0, 6000.0]
+    specs = SG.build_specs(sigmas, 10.0, 6)
+    x = sft.generate_signals(sft.TestSignalKind.SeededNoise, n, 99, 1, sft.Precision.Single)[0]
+    plan = sft.MultiScalePlan(specs, n, 1, out_range)
+    assert plan.describe()["tensor_cores"] == 1 and plan.batch == len(specs)
+    out = plan.empty_output()
+    plan.execute(x, out)
+    for s, sp in enumerate(specs):
+        p1 = sft.TransformPlan(sp, n, 1, 1, out_range, mode="tc")
+        o1 = p1.empty_output()
+        p1.execute(x, o1)
+        torch.cuda.synchronize()
+        assert torch.equal(out[s], o1[0]), f"scale {s}"
+    b = out_range[0] if out_range else 0
+    head = x[:b + 60000].double().cpu().numpy()
+    oh = out.double().cpu().numpy()
+    for s in (0, 3):
+        ref = oracle_transform(O, head, 1, specs[s])[b:b + 30000]
+        assert rel_max(oh[s, :30000, 0] + 1j * oh[s, :30000, 1], ref) < 1e-5
+
+
+def test_multiscale_plan_rejects_mixed_specs(sft):
+    from paper_2110_11866_b200 import scalogram as SG
+
+    specs = SG.build_specs([50.0, 400.0], 10.0, 6)
+    gd = sft.make_gauss_spec(100.0, sft.GaussKind.Value, 6, 2, sft.TransformOptions(precision=0))
+    with pytest.raises(ValueError):
+        sft.MultiScalePlan([specs[0], gd], 100000)
+    f64 = sft.make_transform_spec("MDS2P6", 50.0, 10.0, sft.TransformOptions(precision=1))
+    with pytest.raises(ValueError):
+        sft.MultiScalePlan([f64], 100000)

@@ -7,10 +7,18 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2110_11866_b200 as P
 from paper_2110_11866_b200 import _abi
-B = int(sys.argv[1]) if len(sys.argv) > 1 else 1184
-spec = P.make_transform_spec("MMS5P3", 8192.0, 10.0, P.TransformOptions(precision=0))
-xb = P.generate_signals(P.TestSignalKind.SeededNoise, 102400, 1234, B, P.Precision.Single)
-plan = P.TransformPlan(spec, 102400, B, mode="tc")
+B = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1] != "sg" else 1184
+if len(sys.argv) > 1 and sys.argv[1] == "sg":  # BASELINE config 5: multi-scale plan, 128 scales, N=2^24
+    from paper_2110_11866_b200 import scalogram as SG
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    specs = SG.build_specs(SG.scale_sigmas(128), 10.0, 6,
+                           cache=os.path.join(root, "paper_2110_11866_b200", "data", "scalogram128_xi10_pd6.coef"))
+    xb = P.generate_signals(P.TestSignalKind.SeededNoise, 1 << 24, 1234, 1, P.Precision.Single)[0]
+    plan = P.MultiScalePlan(specs, 1 << 24)
+else:
+    spec = P.make_transform_spec("MMS5P3", 8192.0, 10.0, P.TransformOptions(precision=0))
+    xb = P.generate_signals(P.TestSignalKind.SeededNoise, 102400, 1234, B, P.Precision.Single)
+    plan = P.TransformPlan(spec, 102400, B, mode="tc")
 out = plan.empty_output()
 plan.execute(xb, out)
 tr = torch.zeros(64 * 16, dtype=torch.int64, device="cuda")
