@@ -534,7 +534,14 @@ def run_scalogram(args):
     peak, peak_src = measured_peaks()
     launches_per_step = sc.launches
     kernel_ms = ms / args.steps / max(1, launches_per_step)
-    step_bytes = len(sc.rows) * sc.count * 12
+    # algorithmic bytes: the signal read once per launch (one
+    # multi-scale launch produces all of a rank's scales) + complex64 outputs
+    if sc.multi:
+        step_bytes = sum(n * 4 + p.batch * sc.count * 8 for _, p in sc.multi)
+        kname = f"sft_tc_kernel (K4), {len(sc.multi)} multi-scale launch(es) of <= 128 scales"
+    else:
+        step_bytes = len(sc.rows) * sc.count * 12
+        kname = (kernel_name(sc.plans[0]) + ", one launch per scale") if sc.plans else "none"
     achieved = step_bytes / max(1, launches_per_step) / (kernel_ms * 1e-3) / 1e9
     if rank == 0:
         line = {
@@ -550,8 +557,7 @@ def run_scalogram(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": ncu_traffic("scalogram"), "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": step_bytes / max(1, launches_per_step),
-                         "kernel": kernel_name(sc.plans[0]) + ", one launch per scale" if sc.plans
-                         else "none", "kernel_ms": kernel_ms},
+                         "kernel": kname, "kernel_ms": kernel_ms},
             "e2e": {"value": e2e_value, "unit": "Msamples·scales/s", "h2d_bytes_per_step": n * 4,
                     "d2h_bytes_per_step": sc.output_bytes(), "steps": 1,
                     "path": "Scalogram.run (public API) with pinned host input/output"},
