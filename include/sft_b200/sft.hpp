@@ -378,30 +378,32 @@ inline KernelTaps effective_kernel(const TransformSpec& spec) {
 }
 
 namespace detail {
-template <typename T>
-TransformResult run_transform(const Signal& sig, const TransformSpec& spec) {
+// One call = one library one-shot transform (sftgpu_transform_oneshot): the plan, its
+// device buffers and pinned staging are cached inside the library, so a reference user
+// calling morlet_direct_transform(sig, spec) per signal pays no plan creation per call.
+inline TransformResult transform(const Signal& sig, const TransformSpec& spec) {
   const sftgpu_spec r = spec.synced();
-  Plan plan;
-  check(sftgpu_transform_plan_create(&r, sig.size(), 1, static_cast<int>(sig.boundary), &plan.p));
-  const bool cplx = sftgpu_plan_output_is_complex(plan.p) != 0;
-  std::vector<T> x(sig.samples.begin(), sig.samples.end());
-  std::vector<T> out(static_cast<size_t>(sig.size()) * (cplx ? 2 : 1));
-  check(sftgpu_transform_execute_host(plan.p, x.data(), out.data(), nullptr));
   TransformResult res;
   res.values.resize(static_cast<size_t>(sig.size()));
-  for (size_t i = 0; i < res.values.size(); ++i)
-    res.values[i] = cplx ? std::complex<double>(out[2 * i], out[2 * i + 1]) : std::complex<double>(out[i], 0.0);
-  res.complex_valued = cplx;
+  int cplx = 0;
+  static_assert(sizeof(std::complex<double>) == 2 * sizeof(double), "complex<double> layout");
+  std::vector<double> real;  // real outputs land here, then widen to complex
+  double* out = reinterpret_cast<double*>(res.values.data());
+  const bool maybe_real = spec.kind == TransformKind::Gauss || spec.kind == TransformKind::GaussD ||
+                          spec.kind == TransformKind::GaussDD || spec.kind == TransformKind::TruncConvGauss;
+  if (maybe_real) {
+    real.resize(static_cast<size_t>(sig.size()));
+    out = real.data();
+  }
+  check(sftgpu_transform_oneshot(&r, sig.size(), static_cast<int>(sig.boundary), sig.samples.data(), out, &cplx));
+  if (maybe_real)
+    for (size_t i = 0; i < real.size(); ++i) res.values[i] = std::complex<double>(real[i], 0.0);
+  res.complex_valued = cplx != 0;
   res.abbreviation = spec.abbreviation;
   res.strategy = spec.strategy;
   res.precision = spec.precision;
   res.kernel_rmse_percent = spec.kernel_rmse_percent;
   return res;
-}
-inline TransformResult transform(const Signal& sig, const TransformSpec& spec) {
-  const bool conv = spec.kind == TransformKind::TruncConvGauss || spec.kind == TransformKind::TruncConvMorlet;
-  if (!conv && spec.precision == Precision::Single) return run_transform<float>(sig, spec);
-  return run_transform<double>(sig, spec);
 }
 }  // namespace detail
 

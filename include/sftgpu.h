@@ -268,6 +268,19 @@ int sftgpu_transform_execute_host_async(sftgpu_plan* plan, const void* x_host, v
                                         void* stream);
 /* Blocks until every pipelined call on the plan has finished. */
 int sftgpu_plan_synchronize(sftgpu_plan* plan);
+/* One transform of one fp64 HOST signal, the signature the reference's drop-in calls
+ * need (apply_transform / gauss_smooth / morlet_direct_transform /
+ * morlet_multiply_transform, proj/include/sft/transforms.hpp:86-102, which take an
+ * Eigen::ArrayXd signal and return ArrayXcd values): x_host = n doubles, out_host = n
+ * doubles (real output) or 2n (complex, interleaved re/im); *complex_out tells which.
+ * Plans are cached inside the library per (spec, n, boundary, device), so repeated
+ * calls reuse one plan, its device buffers and its pinned staging (single-precision
+ * specs convert fp64 <-> fp32 on the host, into / out of that staging). Thread-safe (one
+ * call at a time per cached plan). */
+int sftgpu_transform_oneshot(const sftgpu_spec* spec, int64_t n, int boundary, const double* x_host,
+                             double* out_host, int* complex_out);
+/* Drops every cached one-shot plan (frees their device and pinned buffers). */
+void sftgpu_oneshot_cache_clear(void);
 /* 1 if the transform output is complex, 0 if real. */
 int sftgpu_plan_output_is_complex(const sftgpu_plan* plan);
 /* Plan geometry: info[0..10] = {sequential, direct-convolution, positions per thread,

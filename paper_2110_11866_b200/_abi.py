@@ -129,6 +129,8 @@ SIGNATURES = {
     "sftgpu_transform_plan_create": ([C.POINTER(Spec), _I64, _I64, _I, C.POINTER(_P)], _I),
     "sftgpu_transform_plan_create_range": ([C.POINTER(Spec), _I64, _I64, _I, _I64, _I64, C.POINTER(_P)], _I),
     "sftgpu_transform_plan_create_ex": ([C.POINTER(Spec), _I64, _I64, _I, _I64, _I64, _I, C.POINTER(_P)], _I),
+    "sftgpu_transform_oneshot": ([C.POINTER(Spec), _I64, _I, C.c_void_p, C.c_void_p, C.POINTER(_I)], _I),
+    "sftgpu_oneshot_cache_clear": ([], None),
     "sftgpu_multiscale_plan_create": ([C.POINTER(Spec), _I, _I64, _I, _I64, _I64, C.POINTER(_P)], _I),
     "sftgpu_plan_describe": ([_P, C.POINTER(C.c_int64), _I], _I),
     "sftgpu_transform_execute": ([_P, _P, _I64, _P, _I64, _P], _I),

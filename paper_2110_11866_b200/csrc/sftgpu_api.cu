@@ -9,7 +9,9 @@
 #include <cmath>
 #include <complex>
 #include <cstring>
+#include <list>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1744,6 +1746,104 @@ int sftgpu_components_execute_host(sftgpu_plan* pl, const void* x_host, void* c_
 }
 
 void sftgpu_plan_destroy(sftgpu_plan* pl) { delete pl; }
+
+// ---------------------------------------------------------------- one-shot calls
+// Library-owned plan cache for the reference-signature entry points (a reference user
+// calls morlet_direct_transform(sig, spec) per signal; creating a plan per call would cost
+// allocations and a table upload each time).
+extern "C++" {
+namespace {
+struct OneShot {
+  std::string key;
+  sftgpu_plan* plan = nullptr;
+  void* h_x = nullptr;  // pinned staging in the plan's precision
+  void* h_out = nullptr;
+  cudaStream_t st = nullptr;
+  std::mutex mu;
+  ~OneShot() {
+    if (st) cudaStreamSynchronize(st);
+    if (st) cudaStreamDestroy(st);
+    cudaFreeHost(h_x);
+    cudaFreeHost(h_out);
+    delete plan;
+  }
+};
+std::mutex g_oneshot_mu;
+std::list<std::shared_ptr<OneShot>> g_oneshot;  // most recently used first
+constexpr size_t kOneShotMax = 8;
+
+std::shared_ptr<OneShot> oneshot_get(const sftgpu_spec* spec, int64_t n, int boundary) {
+  sftgpu_spec canon;  // canonical bytes (zeroed padding) of the spec's contents
+  spec_to_c(spec_from_c(spec), &canon);
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  std::string key(reinterpret_cast<const char*>(&canon), sizeof(canon));
+  key.append(reinterpret_cast<const char*>(&n), sizeof(n));
+  key.append(reinterpret_cast<const char*>(&boundary), sizeof(boundary));
+  key.append(reinterpret_cast<const char*>(&dev), sizeof(dev));
+  std::lock_guard<std::mutex> lk(g_oneshot_mu);
+  for (auto it = g_oneshot.begin(); it != g_oneshot.end(); ++it)
+    if ((*it)->key == key) {
+      auto e = *it;
+      g_oneshot.erase(it);
+      g_oneshot.push_front(e);
+      return e;
+    }
+  auto e = std::make_shared<OneShot>();
+  e->key = key;
+  const int rc = sftgpu_transform_plan_create(spec, n, 1, boundary, &e->plan);
+  if (rc != SFTGPU_OK) throw ApiError{rc, sftgpu_last_error()};
+  const size_t xb = plan_in_bytes(e->plan), ob = plan_out_bytes(e->plan);
+  cuda_check(cudaHostAlloc(&e->h_x, xb, cudaHostAllocDefault), "cudaHostAlloc one-shot x");
+  cuda_check(cudaHostAlloc(&e->h_out, ob, cudaHostAllocDefault), "cudaHostAlloc one-shot out");
+  cuda_check(cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking), "cudaStreamCreate one-shot");
+  ensure_buffer(&e->plan->d_x, &e->plan->cap_x, xb, "cudaMalloc staging x");
+  ensure_buffer(&e->plan->d_out, &e->plan->cap_out, ob, "cudaMalloc staging out");
+  g_oneshot.push_front(e);
+  if (g_oneshot.size() > kOneShotMax) g_oneshot.pop_back();
+  return e;
+}
+
+// fp64 host signal -> plan precision in pinned staging (host), one H2D, transform, one D2H,
+// -> fp64 (host). Measured alternatives on the B200 box: converting on the device with
+// pageable fp64 copies costs more (the driver stages pageable copies through the host
+// anyway), and chunked copy/convert overlap loses to the per-chunk synchronisation.
+template <typename T>
+void oneshot_run(OneShot& e, const double* x, double* out) {
+  sftgpu_plan* pl = e.plan;
+  const long long n = pl->n, no = static_cast<long long>(plan_out_bytes(pl) / sizeof(T));
+  T* hx = static_cast<T*>(e.h_x);
+  T* ho = static_cast<T*>(e.h_out);
+  for (long long i = 0; i < n; ++i) hx[i] = static_cast<T>(x[i]);
+  cuda_check(cudaMemcpyAsync(pl->d_x, hx, n * sizeof(T), cudaMemcpyHostToDevice, e.st), "H2D");
+  run_transform(pl, pl->d_x, pl->d_out, e.st);
+  cuda_check(cudaMemcpyAsync(ho, pl->d_out, no * sizeof(T), cudaMemcpyDeviceToHost, e.st), "D2H");
+  cuda_check(cudaStreamSynchronize(e.st), "stream sync");
+  for (long long i = 0; i < no; ++i) out[i] = static_cast<double>(ho[i]);
+}
+}  // namespace
+}  // extern "C++"
+
+int sftgpu_transform_oneshot(const sftgpu_spec* spec, int64_t n, int boundary, const double* x_host,
+                             double* out_host, int* complex_out) {
+  return guarded([&] {
+    if (!spec || !x_host || !out_host) fail(SFTGPU_EINVAL, "null argument");
+    if (n < 1) fail(SFTGPU_EINVAL, "Signal: need at least one sample");
+    require_device();
+    std::shared_ptr<OneShot> e = oneshot_get(spec, n, boundary);
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (complex_out) *complex_out = e->plan->mode == sftk::kModeComplex ? 1 : 0;
+    if (e->plan->precision == SFTGPU_SINGLE)
+      oneshot_run<float>(*e, x_host, out_host);
+    else
+      oneshot_run<double>(*e, x_host, out_host);
+  });
+}
+
+void sftgpu_oneshot_cache_clear(void) {
+  std::lock_guard<std::mutex> lk(g_oneshot_mu);
+  g_oneshot.clear();
+}
 
 /* Diagnostics (not part of the reference interface): device buffer of 64 x 16 int64 that
  * K4 fills with per-tile event clocks of CTA 0 (tools/tc_trace.py); NULL disables. */

@@ -737,15 +737,15 @@ class MultiScalePlan(TransformPlan):
 
 
 def _run(sig: Signal, spec: TransformSpec) -> TransformResult:
-    torch = _torch()
-    plan = TransformPlan(spec, sig.size(), 1, sig.boundary)
-    x = torch.from_numpy(sig.samples).to(device="cuda", dtype=plan.dtype())
-    out = plan.empty_output()
-    plan.execute(x, out)
-    torch.cuda.synchronize()
-    o = out[0].double().cpu().numpy()
-    vals = (o[:, 0] + 1j * o[:, 1]) if plan.complex_out else o.astype(np.complex128)
-    return TransformResult(vals, plan.complex_out, spec.abbreviation, spec.strategy, spec.precision,
+    """One reference-signature call (``sftgpu_transform_oneshot``): the library caches the
+    plan, its device buffers and pinned staging per (spec, n, boundary, device)."""
+    x = np.ascontiguousarray(sig.samples, dtype=np.float64)
+    out = np.empty(2 * x.size, dtype=np.float64)
+    cplx = C.c_int(0)
+    check(lib().sftgpu_transform_oneshot(C.byref(spec._raw), x.size, int(sig.boundary), x.ctypes.data_as(C.c_void_p),
+                                         out.ctypes.data_as(C.c_void_p), C.byref(cplx)))
+    vals = out.view(np.complex128) if cplx.value else out[:x.size].astype(np.complex128)
+    return TransformResult(vals, bool(cplx.value), spec.abbreviation, spec.strategy, spec.precision,
                            spec.kernel_rmse_percent)
 
 
