@@ -11,11 +11,15 @@
 // see INTEGRATION.md for the Eigen adapters.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <optional>
+#include <type_traits>
+#include <utility>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -175,14 +179,73 @@ inline ComponentSeq sft_components(const Signal& sig, const SftConfig& cfg) {
 inline ComponentSeq asft_components(const Signal& sig, const SftConfig& cfg) {
   return detail::components(sig, cfg, 0, sig.size() - 1, 2);
 }
-// engine.cpp:323-337: every GPU output is a fresh bounded-state window sum already;
-// the reference's overflow guard for its rebased sequence is kept for API parity.
+// engine.cpp:183-219, 323-337: the sliding-sum route on the GPU (phased sequence, K5
+// flat window sums, rescale / phase removal).
 inline ComponentSeq sft_via_sliding_sum(const Signal& sig, const SftConfig& cfg, int /*workers*/ = 1) {
-  if (cfg.alpha * (0.5 * static_cast<double>(sig.size()) + cfg.half_width) > 600.0)
-    throw std::invalid_argument("sft_via_sliding_sum: alpha * N / 2 too large for the attenuated phased sequence");
+  const sftgpu_config rc = cfg.raw();
+  ComponentSeq out{ArrayXd(static_cast<size_t>(sig.size())), ArrayXd(static_cast<size_t>(sig.size()))};
+  detail::check(sftgpu_sft_via_sliding_sum(&rc, sig.samples.data(), sig.size(), static_cast<int>(sig.boundary),
+                                           out.c.data(), out.s.data()));
+  return out;
+}
+
+
+// engine.hpp:82-102 --------------------------------------------------------------------
+/// Kernel-integral window state u_{(2K+1)}[n+K] = sum_{j=n-K}^{n+K} x[j] e^{i omega j}
+/// two ways (engine.cpp:270-300), both on the GPU: via_prefix by the sliding-sum route
+/// (K5 window sums of the phased sequence), via_recurrence by the window-recurrence scan
+/// (K1); each GPU result carries the output phase removed, re-applied here. Plain SFT only.
+struct WindowState {
+  ArrayXcd via_prefix;
+  ArrayXcd via_recurrence;
+};
+inline WindowState sliding_window_state(const Signal& sig, const SftConfig& cfg) {
+  if (cfg.alpha != 0.0) throw std::invalid_argument("sliding_window_state: plain SFT only");
   SftConfig k = cfg;
   k.strategy = Strategy::KernelIntegral;
-  return detail::components(sig, k, 0, sig.size() - 1, 0);
+  k.precision = Precision::Double;
+  const ComponentSeq a = sft_via_sliding_sum(sig, k);
+  const ComponentSeq b = sft_components(sig, k);
+  const double omega = cfg.order.integer_order ? cfg.beta * cfg.order.p : cfg.order.omega;
+  WindowState st;
+  st.via_prefix.resize(a.c.size());
+  st.via_recurrence.resize(b.c.size());
+  for (size_t n = 0; n < a.c.size(); ++n) {
+    const std::complex<double> ph(std::cos(omega * static_cast<double>(n)), std::sin(omega * static_cast<double>(n)));
+    st.via_prefix[n] = ph * std::complex<double>(a.c[n], -a.s[n]);
+    st.via_recurrence[n] = ph * std::complex<double>(b.c[n], -b.s[n]);
+  }
+  return st;
+}
+
+/// engine.cpp:302-320: cfg at single precision against a double-precision run of the same
+/// configuration (both on the GPU). abs_error[n] = max(|dc|, |ds|); max_component_error is
+/// its max over the reference's peak component. max_state_magnitude is the peak |window
+/// state| the fp32 scan carries (the GPU keeps the 2K-window state, not the reference's
+/// running recursion).
+struct StabilityReport {
+  double max_state_magnitude = 0.0;
+  double max_component_error = 0.0;
+  double reference_scale = 0.0;
+  ArrayXd abs_error;
+};
+inline StabilityReport stability_probe(const Signal& sig, const SftConfig& cfg) {
+  SftConfig sc = cfg, dc = cfg;
+  sc.precision = Precision::Single;
+  dc.precision = Precision::Double;
+  const ComponentSeq lo = components_over(sig, sc, 0, sig.size() - 1);
+  const ComponentSeq ref = components_over(sig, dc, 0, sig.size() - 1);
+  StabilityReport r;
+  r.abs_error.resize(ref.c.size());
+  double emax = 0.0;
+  for (size_t n = 0; n < ref.c.size(); ++n) {
+    r.abs_error[n] = std::max(std::abs(lo.c[n] - ref.c[n]), std::abs(lo.s[n] - ref.s[n]));
+    emax = std::max(emax, r.abs_error[n]);
+    r.reference_scale = std::max({r.reference_scale, std::abs(ref.c[n]), std::abs(ref.s[n])});
+    r.max_state_magnitude = std::max(r.max_state_magnitude, std::hypot(lo.c[n], lo.s[n]));
+  }
+  r.max_component_error = r.reference_scale > 0.0 ? emax / r.reference_scale : emax;
+  return r;
 }
 
 // ------------------------------------------------------------------ kernels (kernels.hpp)
@@ -445,6 +508,316 @@ inline double morlet_multiply_kernel_rmse(const MorletParams& p, int pm, int n0)
   double r = 0.0;
   detail::check(sftgpu_morlet_multiply_kernel_rmse(p.sigma, p.xi, p.half_width, pm, n0, &r));
   return r;
+}
+
+// fourier_fit.hpp:14-160 ---------------------------------------------------------------
+struct HarmonicGrid {
+  int half_width;
+  double beta;
+  std::vector<int> cos_orders;
+  std::vector<int> sin_orders;
+  HarmonicGrid(int k, double beta_, std::vector<int> cos_p, std::vector<int> sin_p)
+      : half_width(k), beta(beta_), cos_orders(std::move(cos_p)), sin_orders(std::move(sin_p)) {}
+  std::size_t basis_size() const { return cos_orders.size() + sin_orders.size(); }
+};
+enum class CoeffKind { GaussCos = 0, GaussDerivSin, GaussDeriv2Cos, MorletDirect, MorletMultiply };
+struct CoefficientSet {
+  CoeffKind kind = CoeffKind::GaussCos;
+  HarmonicGrid grid{1, 1.0, {}, {}};
+  ArrayXcd cos_coeffs;
+  ArrayXcd sin_coeffs;
+  double fit_rmse_percent = 0.0;
+  double sigma = 0.0;
+  double xi = 0.0;
+  int n0 = 0;
+
+  static CoefficientSet from_raw(const sftgpu_coeffs& r) {
+    CoefficientSet c;
+    c.kind = static_cast<CoeffKind>(r.kind);
+    c.grid = HarmonicGrid(r.half_width, r.beta, std::vector<int>(r.cos_orders, r.cos_orders + r.n_cos),
+                          std::vector<int>(r.sin_orders, r.sin_orders + r.n_sin));
+    for (int i = 0; i < r.n_cos; ++i) c.cos_coeffs.emplace_back(r.cos_coeffs[2 * i], r.cos_coeffs[2 * i + 1]);
+    for (int i = 0; i < r.n_sin; ++i) c.sin_coeffs.emplace_back(r.sin_coeffs[2 * i], r.sin_coeffs[2 * i + 1]);
+    c.fit_rmse_percent = r.fit_rmse_percent;
+    c.sigma = r.sigma;
+    c.xi = r.xi;
+    c.n0 = r.n0;
+    return c;
+  }
+  sftgpu_coeffs raw() const {
+    sftgpu_coeffs r;
+    std::memset(&r, 0, sizeof(r));
+    if (grid.cos_orders.size() > SFTGPU_MAX_COEFFS || grid.sin_orders.size() > SFTGPU_MAX_COEFFS)
+      throw std::invalid_argument("CoefficientSet: too many orders");
+    r.kind = static_cast<int>(kind);
+    r.half_width = grid.half_width;
+    r.beta = grid.beta;
+    r.n_cos = static_cast<int>(grid.cos_orders.size());
+    r.n_sin = static_cast<int>(grid.sin_orders.size());
+    for (int i = 0; i < r.n_cos; ++i) {
+      r.cos_orders[i] = grid.cos_orders[i];
+      r.cos_coeffs[2 * i] = i < static_cast<int>(cos_coeffs.size()) ? cos_coeffs[i].real() : 0.0;
+      r.cos_coeffs[2 * i + 1] = i < static_cast<int>(cos_coeffs.size()) ? cos_coeffs[i].imag() : 0.0;
+    }
+    for (int i = 0; i < r.n_sin; ++i) {
+      r.sin_orders[i] = grid.sin_orders[i];
+      r.sin_coeffs[2 * i] = i < static_cast<int>(sin_coeffs.size()) ? sin_coeffs[i].real() : 0.0;
+      r.sin_coeffs[2 * i + 1] = i < static_cast<int>(sin_coeffs.size()) ? sin_coeffs[i].imag() : 0.0;
+    }
+    r.fit_rmse_percent = fit_rmse_percent;
+    r.sigma = sigma;
+    r.xi = xi;
+    r.n0 = n0;
+    return r;
+  }
+};
+
+/// fit_mmse (fourier_fit.cpp:67-105): least squares on the nodes [-K, K]; a real target
+/// is the complex one with zero imaginary part.
+inline CoefficientSet fit_mmse(const ArrayXcd& target, const HarmonicGrid& grid, CoeffKind kind) {
+  std::vector<double> t(2 * target.size());
+  for (size_t i = 0; i < target.size(); ++i) {
+    t[2 * i] = target[i].real();
+    t[2 * i + 1] = target[i].imag();
+  }
+  if (target.size() != static_cast<size_t>(2 * grid.half_width + 1))
+    throw std::invalid_argument("fit_mmse: target size must be 2K+1");
+  sftgpu_coeffs r;
+  detail::check(sftgpu_fit_mmse(t.data(), grid.half_width, grid.beta, static_cast<int>(grid.cos_orders.size()),
+                                grid.cos_orders.data(), static_cast<int>(grid.sin_orders.size()),
+                                grid.sin_orders.data(), static_cast<int>(kind), &r));
+  return CoefficientSet::from_raw(r);
+}
+inline CoefficientSet fit_mmse(const ArrayXd& target, const HarmonicGrid& grid, CoeffKind kind) {
+  return fit_mmse(ArrayXcd(target.begin(), target.end()), grid, kind);
+}
+
+/// reconstruct (fourier_fit.cpp:107-129): the fitted series at arbitrary points.
+inline ArrayXcd reconstruct(const CoefficientSet& coeffs, const ArrayXd& points) {
+  const sftgpu_coeffs r = coeffs.raw();
+  ArrayXcd out(points.size());
+  detail::check(sftgpu_reconstruct(&r, points.data(), static_cast<std::int64_t>(points.size()),
+                                   reinterpret_cast<double*>(out.data())));
+  return out;
+}
+
+struct GaussianFitBundle {
+  GaussianParams params{1.0, 1};
+  double beta = 0.0;
+  int max_order = 0;
+  ArrayXd a, b, d;
+  double fit_rmse_g = 0.0, fit_rmse_gd = 0.0, fit_rmse_gdd = 0.0;
+};
+inline GaussianFitBundle fit_gaussian_bundle(const GaussianParams& params, int max_order, double beta) {
+  sftgpu_gauss_bundle r;
+  detail::check(sftgpu_fit_gaussian_bundle(params.sigma, params.half_width, max_order, beta, &r));
+  GaussianFitBundle g;
+  g.params = params;
+  g.beta = r.beta;
+  g.max_order = r.max_order;
+  g.a.assign(r.a, r.a + r.max_order + 1);
+  g.b.assign(r.b, r.b + r.max_order);
+  g.d.assign(r.d, r.d + r.max_order + 1);
+  g.fit_rmse_g = r.fit_rmse_g;
+  g.fit_rmse_gd = r.fit_rmse_gd;
+  g.fit_rmse_gdd = r.fit_rmse_gdd;
+  return g;
+}
+inline double gauss_kernel_rmse(const GaussianFitBundle& bundle, GaussKind kind, int n0) {
+  sftgpu_gauss_bundle r;
+  std::memset(&r, 0, sizeof(r));
+  r.sigma = bundle.params.sigma;
+  r.half_width = bundle.params.half_width;
+  r.beta = bundle.beta;
+  r.max_order = bundle.max_order;
+  std::copy(bundle.a.begin(), bundle.a.end(), r.a);
+  std::copy(bundle.b.begin(), bundle.b.end(), r.b);
+  std::copy(bundle.d.begin(), bundle.d.end(), r.d);
+  double v = 0.0;
+  detail::check(sftgpu_gauss_kernel_rmse(&r, static_cast<int>(kind), n0, &v));
+  return v;
+}
+inline CoefficientSet fit_morlet_direct(const MorletParams& params, int ps, int pd, double beta, int n0 = 0) {
+  sftgpu_coeffs r;
+  detail::check(sftgpu_fit_morlet_direct(params.sigma, params.xi, params.half_width, ps, pd, beta, n0, &r));
+  return CoefficientSet::from_raw(r);
+}
+inline CoefficientSet fit_morlet_envelope(const MorletParams& params, int max_order, double beta) {
+  sftgpu_coeffs r;
+  detail::check(sftgpu_fit_morlet_envelope(params.sigma, params.xi, params.half_width, max_order, beta, &r));
+  return CoefficientSet::from_raw(r);
+}
+
+struct BetaTuneResult {
+  double beta = 0.0;
+  double rmse_percent = 0.0;
+};
+/// tune_beta (fourier_fit.cpp:395-438) over any RMSE profile.
+inline BetaTuneResult tune_beta(const std::function<double(double)>& rmse_of_beta, int half_width) {
+  auto tramp = [](double beta, void* u) { return (*static_cast<const std::function<double(double)>*>(u))(beta); };
+  BetaTuneResult r;
+  detail::check(sftgpu_tune_beta(tramp, const_cast<std::function<double(double)>*>(&rmse_of_beta), half_width,
+                                 &r.beta, &r.rmse_percent));
+  return r;
+}
+inline BetaTuneResult tune_beta_gauss(const GaussianParams& params, int max_order, int n0 = 0) {
+  BetaTuneResult r;
+  detail::check(sftgpu_tune_beta_gauss(params.sigma, params.half_width, max_order, n0, &r.beta, &r.rmse_percent));
+  return r;
+}
+
+// sliding_sum.hpp ----------------------------------------------------------------------
+enum class SsVariant { FlatDoubling, Blocked8 };
+/// Round / stage schedule of the data-parallel sliding sum (sliding_sum.hpp:23-64).
+struct SlidingSumPlan {
+  std::int64_t input_size = 0, window = 0;
+  int rounds = 0;
+  SsVariant variant = SsVariant::FlatDoubling;
+  std::int64_t core_budget = 1;
+  std::int64_t padded_size = 0;
+  int block_rows = 16, block_cols = 8;
+  static SlidingSumPlan make(std::int64_t n, std::int64_t window, SsVariant variant = SsVariant::FlatDoubling,
+                             std::int64_t core_budget = 1) {
+    if (core_budget < 1) throw std::invalid_argument("SlidingSumPlan: M must be >= 1");
+    std::int64_t info[5];
+    detail::check(sftgpu_sliding_sum_plan(n, window, variant == SsVariant::Blocked8, info));
+    SlidingSumPlan p;
+    p.input_size = n;
+    p.window = window;
+    p.variant = variant;
+    p.core_budget = core_budget;
+    p.rounds = static_cast<int>(info[0]);
+    p.padded_size = info[1];
+    return p;
+  }
+  int blocked_stages() const { return blocked_stages_for(window); }
+  static int blocked_stages_for(std::int64_t window) {
+    int st = 0;
+    for (std::int64_t rest = window; rest > 0; rest /= 8) ++st;
+    return st;
+  }
+};
+struct RoundRecord {
+  int round = 0, stage = 0, r = 0, bit = 0;
+  std::int64_t active = 0, adds = 0;
+};
+struct RoundTrace {
+  std::vector<RoundRecord> rounds;
+  std::int64_t total_adds() const {
+    std::int64_t t = 0;
+    for (const auto& rec : rounds) t += rec.adds;
+    return t;
+  }
+};
+namespace detail {
+// the rounds the GPU kernels execute (K5: flat doubling; K6: three rounds per base-8 digit)
+inline void fill_trace(const SlidingSumPlan& p, RoundTrace* tr) {
+  if (!tr) return;
+  tr->rounds.clear();
+  if (p.variant == SsVariant::FlatDoubling) {
+    for (int r = 0; r < p.rounds; ++r) {
+      const int b = static_cast<int>((p.window >> r) & 1);
+      tr->rounds.push_back({r, 0, r, b, p.input_size, p.input_size * (1 + b)});
+    }
+    return;
+  }
+  std::int64_t rows = p.padded_size, cols = 1, rest = p.window;
+  int g = 0, stage = 0;
+  while (rest > 0) {
+    const std::int64_t blocks = ((rows + 63) / 64) * cols;
+    for (int r = 0; r < 3; ++r) {
+      const int b = static_cast<int>((rest >> r) & 1);
+      const std::int64_t active = static_cast<std::int64_t>(16 - (1 << r)) * 8 * blocks;
+      tr->rounds.push_back({g++, stage, r, b, active, active * (1 + b)});
+    }
+    rows /= 8;
+    cols *= 8;
+    rest /= 8;
+    ++stage;
+  }
+}
+template <typename T>
+constexpr int ss_dtype() {
+  if constexpr (std::is_same<T, std::int64_t>::value) return SFTGPU_SS_I64;
+  else if constexpr (std::is_same<T, double>::value) return SFTGPU_SS_F64;
+  else {
+    static_assert(std::is_same<T, std::complex<double>>::value, "sliding sums: int64, double or complex<double>");
+    return SFTGPU_SS_C128;
+  }
+}
+template <typename T>
+std::vector<T> sliding_sum(const std::vector<T>& f, std::int64_t window, bool blocked, RoundTrace* trace) {
+  const SlidingSumPlan p = SlidingSumPlan::make(static_cast<std::int64_t>(f.size()), window,
+                                                blocked ? SsVariant::Blocked8 : SsVariant::FlatDoubling);
+  std::vector<T> out(f.size() - static_cast<size_t>(window) + 1);
+  check(sftgpu_sliding_sum_host(ss_dtype<T>(), blocked ? 1 : 0, f.data(), static_cast<std::int64_t>(f.size()), window,
+                                out.data()));
+  fill_trace(p, trace);
+  return out;
+}
+}  // namespace detail
+/// Paper Algorithm 1 (sliding_sum.hpp:89-121) on the GPU (K5), bit-identical addition trees.
+template <typename T>
+std::vector<T> sliding_sum_flat(const std::vector<T>& f, std::int64_t window, int /*workers*/ = 1,
+                                RoundTrace* trace = nullptr) {
+  return detail::sliding_sum(f, window, false, trace);
+}
+/// Paper Algorithms 2-3 (sliding_sum.hpp:144-234) on the GPU (K6), bit-identical addition trees.
+template <typename T>
+std::vector<T> sliding_sum_blocked8(const std::vector<T>& f, std::int64_t window, int /*workers*/ = 1,
+                                    RoundTrace* trace = nullptr) {
+  return detail::sliding_sum(f, window, true, trace);
+}
+inline std::pair<std::int64_t, std::int64_t> blocked8_layout(std::int64_t index, int stages) {
+  std::int64_t div = 1;
+  for (int t = 0; t < stages; ++t) div *= 8;
+  std::int64_t rem = index % div, col = 0;
+  for (int t = 0; t < stages; ++t) {
+    col = col * 8 + rem % 8;
+    rem /= 8;
+  }
+  return {index / div, col};
+}
+
+struct CostReport {
+  std::int64_t parallel_steps = 0;
+  int outer_iterations = 0;
+  std::int64_t total_adds = 0;
+  std::int64_t total_mults = 0;
+  std::string predicted_regime;
+};
+/// cost_model (src/sliding_sum.cpp:7-40): exact operation counts of a plan's rounds.
+inline CostReport cost_model(const SlidingSumPlan& plan) {
+  std::int64_t info[5];
+  detail::check(sftgpu_sliding_sum_plan(plan.input_size, plan.window, plan.variant == SsVariant::Blocked8, info));
+  CostReport r;
+  r.parallel_steps = info[3];
+  r.outer_iterations = plan.variant == SsVariant::Blocked8 ? plan.blocked_stages() : 1;
+  r.total_adds = info[4];
+  r.total_mults = 0;
+  r.predicted_regime = plan.core_budget >= plan.input_size ? "O(log2 L) parallel time (M >= N)"
+                                                           : "O(N log2 L / M) parallel time (M < N)";
+  return r;
+}
+struct MethodOpCounts {
+  std::int64_t mults = 0, adds = 0;
+  std::string regime;
+};
+/// src/sliding_sum.cpp:42-66: method-level operation counts of the benchmark comparisons.
+inline MethodOpCounts sft_method_counts(std::int64_t n, int orders, std::int64_t half_width, std::int64_t core_budget) {
+  MethodOpCounts c;
+  c.mults = 7 * n * orders;
+  c.adds = n * orders * (2 * half_width + 1);
+  c.regime = core_budget >= n ? "O(P log2 K) time (M >= N)" : "O(N P log2 K / M) time (M < N)";
+  return c;
+}
+inline MethodOpCounts conv_method_counts(std::int64_t n, double sigma, std::int64_t core_budget) {
+  MethodOpCounts c;
+  const std::int64_t window = static_cast<std::int64_t>(std::llround(6.0 * sigma)) + 1;
+  c.mults = n * window;
+  c.adds = n * window;
+  c.regime = core_budget >= c.adds ? "O(log2 sigma) time (M >= N(6 sigma + 1))" : "O(N sigma log2 sigma / M) time";
+  return c;
 }
 
 }  // namespace sft

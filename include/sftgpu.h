@@ -203,6 +203,13 @@ int sftgpu_gauss_kernel_rmse(const sftgpu_gauss_bundle* b, int gauss_kind, int n
                              double* rmse);
 int sftgpu_tune_beta_gauss(double sigma, int half_width, int max_order, int n0,
                            double* beta, double* rmse);
+/* tune_beta (src/fourier_fit.cpp:395-438): 33-point prescan of rmse_of_beta over
+ * [0.5 pi/K, 1.5 pi/K], then golden section to 1e-4 relative. */
+int sftgpu_tune_beta(double (*rmse_of_beta)(double beta, void* user), void* user, int half_width,
+                     double* beta, double* rmse);
+/* reconstruct (src/fourier_fit.cpp:107-129): the fitted series at n points, complex
+ * values interleaved (re, im) into out_re_im[2n]. */
+int sftgpu_reconstruct(const sftgpu_coeffs* coeffs, const double* points, int64_t n, double* out_re_im);
 
 /* Coefficient files, "sft-coefficients v1" text format
  * (replaces write_coefficient_sets / read_coefficient_sets, src/coeff_io.cpp:21-101). */
@@ -327,8 +334,16 @@ int sftgpu_truncated_convolution(const double* x, int64_t n, int boundary,
 enum { SFTGPU_SS_I64 = 0, SFTGPU_SS_F64 = 1, SFTGPU_SS_C128 = 2 };
 int sftgpu_sliding_sum_plan(int64_t n, int64_t L, int blocked, int64_t* info);
 int sftgpu_sliding_sum(int dtype, int blocked, const void* f, int64_t n, int64_t L, void* out, void* stream);
+/* sft_via_sliding_sum (src/engine.cpp:183-219, 323-337): the components of one SftConfig
+ * over the whole signal by the reference's sliding-sum route, on the GPU: the rebased
+ * phased sequence, the K5 flat window sums (paper Algorithm 1, complex128), rescale and
+ * phase removal. HOST fp64 signal in, c = Re / s = -Im out (n each); synchronous. The
+ * same argument checks as the reference (alpha * N / 2 > 600 rejected). */
+int sftgpu_sft_via_sliding_sum(const sftgpu_config* cfg, const double* x_host, int64_t n, int boundary,
+                               double* c_host, double* s_host);
 
 /* Host-memory variants (device buffers managed internally; synchronous). */
+int sftgpu_sliding_sum_host(int dtype, int blocked, const void* f_host, int64_t n, int64_t L, void* out_host);
 int sftgpu_generate_signal_host(int kind, int64_t n, uint64_t seed, double* out_host);
 int sftgpu_truncated_convolution_host(const double* x_host, int64_t n, int boundary,
                                       const double* taps_host, int64_t n_taps, int64_t tap_lo,

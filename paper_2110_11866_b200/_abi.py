@@ -147,6 +147,11 @@ SIGNATURES = {
     "sftgpu_truncated_convolution_host": ([_P, _I64, _I, _P, _I64, _I64, _P], _I),
     "sftgpu_sliding_sum_plan": ([_I64, _I64, _I, C.POINTER(C.c_int64)], _I),
     "sftgpu_sliding_sum": ([_I, _I, _P, _I64, _I64, _P, _P], _I),
+    "sftgpu_sliding_sum_host": ([_I, _I, C.c_void_p, _I64, _I64, C.c_void_p], _I),
+    "sftgpu_tune_beta": ([C.CFUNCTYPE(C.c_double, C.c_double, C.c_void_p), C.c_void_p, _I, C.POINTER(C.c_double),
+                          C.POINTER(C.c_double)], _I),
+    "sftgpu_reconstruct": ([C.POINTER(Coeffs), C.c_void_p, _I64, C.c_void_p], _I),
+    "sftgpu_sft_via_sliding_sum": ([C.POINTER(Config), C.c_void_p, _I64, _I, C.c_void_p, C.c_void_p], _I),
     "sftgpu_generate_signal": ([_I, _I64, _U64, _I64, _I, _P, _P], _I),
     "sftgpu_truncated_convolution": ([_P, _I64, _I, _P, _I64, _I64, _P, _P], _I),
 }

@@ -579,6 +579,10 @@ BetaTune tune_beta(F&& f, int K) {
   return r;
 }
 
+BetaTune tune_beta_callback(double (*f)(double, void*), void* user, int K) {
+  return tune_beta([&](double beta) { return f(beta, user); }, K);
+}
+
 BetaTune tune_beta_gauss(const GaussP& p, int P, int n0) {
   return tune_beta(
       [&](double beta) { return gauss_kernel_rmse(fit_gaussian_bundle(p, P, beta), GKind::Value, n0); },

@@ -97,6 +97,8 @@ struct BetaTune {
   double beta = 0, rmse = 0;
 };
 BetaTune tune_beta_gauss(const GaussP& p, int P, int n0);
+// tune_beta (proj/src/fourier_fit.cpp:395-438) over a caller-supplied RMSE profile
+BetaTune tune_beta_callback(double (*f)(double, void*), void* user, int K);
 
 // TransformSpec (proj/include/sft/transforms.hpp:23-41)
 struct Options {

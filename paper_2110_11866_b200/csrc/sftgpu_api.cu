@@ -1308,6 +1308,30 @@ int sftgpu_tune_beta_gauss(double sigma, int K, int P, int n0, double* beta, dou
   });
 }
 
+int sftgpu_tune_beta(double (*rmse_of_beta)(double beta, void* user), void* user, int half_width, double* beta,
+                     double* rmse) {
+  return guarded([&] {
+    if (!rmse_of_beta || !beta || !rmse) fail(SFTGPU_EINVAL, "null argument");
+    if (half_width < 1) fail(SFTGPU_EINVAL, "tune_beta: K must be >= 1");
+    const sftb::BetaTune r = sftb::tune_beta_callback(rmse_of_beta, user, half_width);
+    *beta = r.beta;
+    *rmse = r.rmse;
+  });
+}
+
+int sftgpu_reconstruct(const sftgpu_coeffs* coeffs, const double* points, int64_t n, double* out_re_im) {
+  return guarded([&] {
+    if (!coeffs || (!points && n > 0) || (!out_re_im && n > 0)) fail(SFTGPU_EINVAL, "null argument");
+    const sftb::Coeffs c = coeffs_from_c(coeffs);
+    const std::vector<double> q(points, points + n);
+    const std::vector<cd> v = sftb::reconstruct(c, q);
+    for (int64_t i = 0; i < n; ++i) {
+      out_re_im[2 * i] = v[i].real();
+      out_re_im[2 * i + 1] = v[i].imag();
+    }
+  });
+}
+
 int sftgpu_write_coefficient_sets(const char* path, const sftgpu_coeffs* sets, int n_sets) {
   return guarded([&] {
     if (!path || (!sets && n_sets > 0)) fail(SFTGPU_EINVAL, "null argument");

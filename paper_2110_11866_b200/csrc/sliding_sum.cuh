@@ -106,4 +106,43 @@ __global__ void sliding_blocked8_gather(const T* __restrict__ h, T* __restrict__
   }
 }
 
+// Sliding-sum route of the components (proj/src/engine.cpp:183-219): the attenuated,
+// phased sequence f[i] = x_ext[j] e^{alpha (j - center)} e^{i omega j}, j = lo - K + i,
+// rebased at the window center so that e^{+-alpha ...} stays in range; then the window
+// sums of K5; then each output is rescaled and its phase removed.
+__device__ __forceinline__ double ext_sample(const double* x, long long n, int boundary, long long j) {
+  if (j >= 0 && j < n) return x[j];
+  if (boundary == 0) return 0.0;
+  return j < 0 ? x[0] : x[n - 1];
+}
+__global__ void phased_sequence_kernel(const double* __restrict__ x, long long n, int boundary, long long lo,
+                                       int K, double omega, double alpha, double center, long long len,
+                                       double2* __restrict__ f) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < len;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long j = lo - K + i;
+    const double w = alpha == 0.0 ? 1.0 : exp(alpha * (static_cast<double>(j) - center));
+    const double xj = ext_sample(x, n, boundary, j) * w;
+    double sn, cs;
+    sincos(omega * static_cast<double>(j), &sn, &cs);
+    f[i] = make_double2(xj * cs, xj * sn);
+  }
+}
+__global__ void sliding_route_output_kernel(const double2* __restrict__ sums, long long lo, long long count,
+                                            double omega, double alpha, double center, double* __restrict__ c,
+                                            double* __restrict__ s) {
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < count;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long nn = lo + k;
+    const double2 w = sums[k];
+    const double scale = alpha == 0.0 ? 1.0 : exp(-alpha * (static_cast<double>(nn) - center));
+    double sn, cs;
+    sincos(omega * static_cast<double>(nn), &sn, &cs);
+    // remove_phase (engine.cpp:129-134), stored as c = Re, s = -Im (ComponentSink)
+    const double re = w.x * cs + w.y * sn, im = w.y * cs - w.x * sn;
+    c[k] = scale * re;
+    s[k] = -scale * im;
+  }
+}
+
 }  // namespace sftk

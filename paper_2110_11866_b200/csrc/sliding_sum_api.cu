@@ -159,3 +159,129 @@ extern "C" int sftgpu_sliding_sum(int dtype, int blocked, const void* f, int64_t
     default: sftgpu_set_error("sliding sum: unknown dtype"); return SFTGPU_EINVAL;
   }
 }
+
+// sft_via_sliding_sum (proj/src/engine.cpp:183-219, 323-337): the reference's sliding-sum
+// route for one SftConfig, on the GPU: phased sequence, K5 flat window sums (paper
+// Algorithm 1, complex128), rescale and phase removal. Host fp64 in / out, synchronous.
+// The GPU route accumulates in fp64 for both precisions (the reference sums complex<float>
+// for Single; the parity bar is the fp64 result).
+extern "C" int sftgpu_sft_via_sliding_sum(const sftgpu_config* cfg, const double* x_host, int64_t n, int boundary,
+                                          double* c_host, double* s_host) {
+  if (!cfg || !x_host || !c_host || !s_host) {
+    sftgpu_set_error("sft_via_sliding_sum: null argument");
+    return SFTGPU_EINVAL;
+  }
+  if (n < 1) {
+    sftgpu_set_error("Signal: need at least one sample");
+    return SFTGPU_EINVAL;
+  }
+  if (cfg->half_width < 1) {
+    sftgpu_set_error("SftConfig: K must be >= 1");
+    return SFTGPU_EINVAL;
+  }
+  if (cfg->integer_order && !(cfg->beta > 0.0)) {
+    sftgpu_set_error("SftConfig: beta must be > 0");
+    return SFTGPU_EINVAL;
+  }
+  if (cfg->alpha < 0.0) {
+    sftgpu_set_error("SftConfig: alpha must be >= 0");
+    return SFTGPU_EINVAL;
+  }
+  if (cfg->integer_order && cfg->p < 0) {
+    sftgpu_set_error("OrderSpec: p must be >= 0");
+    return SFTGPU_EINVAL;
+  }
+  if (boundary != SFTGPU_BOUNDARY_ZERO && boundary != SFTGPU_BOUNDARY_CLAMP) {
+    sftgpu_set_error("unknown boundary policy");
+    return SFTGPU_EINVAL;
+  }
+  const long long K = cfg->half_width, lo = 0, hi = n - 1, count = n, len = count + 2 * K;
+  const double omega = cfg->integer_order ? cfg->beta * cfg->p : cfg->omega;
+  const double center = 0.5 * static_cast<double>(lo + hi);
+  if (cfg->alpha * (0.5 * static_cast<double>(count) + K) > 600.0) {
+    sftgpu_set_error("sft_via_sliding_sum: alpha * N / 2 too large for the attenuated phased sequence");
+    return SFTGPU_EINVAL;
+  }
+  int devs = 0;
+  if (cudaGetDeviceCount(&devs) != cudaSuccess || devs == 0) {
+    sftgpu_set_error("no CUDA device available (libsftgpu has no CPU fallback)");
+    return SFTGPU_ECUDA;
+  }
+  SsPlan p;
+  if (!make_plan(len, 2 * K + 1, &p)) return SFTGPU_EINVAL;
+  double* dx = nullptr;
+  double2 *f = nullptr, *sums = nullptr;
+  double *dc = nullptr, *ds = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(dx);
+    cudaFree(f);
+    cudaFree(sums);
+    cudaFree(dc);
+    cudaFree(ds);
+  };
+  auto cuda_fail = [&](cudaError_t e) {
+    cleanup();
+    sftgpu_set_error(std::string("sft_via_sliding_sum: ") + cudaGetErrorString(e));
+    return SFTGPU_ECUDA;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&dx, n * sizeof(double))) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaMalloc(&f, len * sizeof(double2))) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaMalloc(&sums, count * sizeof(double2))) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaMalloc(&dc, count * sizeof(double))) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaMalloc(&ds, count * sizeof(double))) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaMemcpy(dx, x_host, n * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess) return cuda_fail(e);
+  const int sms = sftk::sm_count();
+  sftk::phased_sequence_kernel<<<4 * sms, 256>>>(dx, n, boundary, lo, static_cast<int>(K), omega, cfg->alpha, center,
+                                                 len, f);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e);
+  const int rc = run<double2>(0, f, p, sums, nullptr);
+  if (rc != SFTGPU_OK) {
+    cleanup();
+    return rc;
+  }
+  sftk::sliding_route_output_kernel<<<4 * sms, 256>>>(sums, lo, count, omega, cfg->alpha, center, dc, ds);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaMemcpy(c_host, dc, count * sizeof(double), cudaMemcpyDeviceToHost)) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaMemcpy(s_host, ds, count * sizeof(double), cudaMemcpyDeviceToHost)) != cudaSuccess) return cuda_fail(e);
+  cleanup();
+  return SFTGPU_OK;
+}
+
+// Host-memory variant of sftgpu_sliding_sum (device buffers managed here; synchronous).
+extern "C" int sftgpu_sliding_sum_host(int dtype, int blocked, const void* f_host, int64_t n, int64_t L,
+                                       void* out_host) {
+  SsPlan p;
+  if (!make_plan(n, L, &p)) return SFTGPU_EINVAL;
+  if (!f_host || !out_host) {
+    sftgpu_set_error("sliding sum: null buffer");
+    return SFTGPU_EINVAL;
+  }
+  const size_t es = dtype == SFTGPU_SS_C128 ? 16 : 8;
+  if (dtype != SFTGPU_SS_I64 && dtype != SFTGPU_SS_F64 && dtype != SFTGPU_SS_C128) {
+    sftgpu_set_error("sliding sum: unknown dtype");
+    return SFTGPU_EINVAL;
+  }
+  int devs = 0;
+  if (cudaGetDeviceCount(&devs) != cudaSuccess || devs == 0) {
+    sftgpu_set_error("no CUDA device available (libsftgpu has no CPU fallback)");
+    return SFTGPU_ECUDA;
+  }
+  void *df = nullptr, *dout = nullptr;
+  const size_t count = static_cast<size_t>(n - L + 1);
+  cudaError_t e = cudaMalloc(&df, static_cast<size_t>(n) * es);
+  if (e == cudaSuccess) e = cudaMalloc(&dout, count * es);
+  if (e == cudaSuccess) e = cudaMemcpy(df, f_host, static_cast<size_t>(n) * es, cudaMemcpyHostToDevice);
+  int rc = SFTGPU_OK;
+  if (e == cudaSuccess) {
+    rc = sftgpu_sliding_sum(dtype, blocked, df, n, L, dout, nullptr);
+    if (rc == SFTGPU_OK) e = cudaMemcpy(out_host, dout, count * es, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(df);
+  cudaFree(dout);
+  if (e != cudaSuccess) {
+    sftgpu_set_error(std::string("sliding sum: ") + cudaGetErrorString(e));
+    return SFTGPU_ECUDA;
+  }
+  return rc;
+}

@@ -29,6 +29,8 @@ __all__ = [
     "truncated_convolution", "fit_gaussian_bundle", "fit_morlet_direct", "fit_morlet_envelope",
     "fit_mmse", "select_optimal_ps", "tune_beta_gauss", "gauss_kernel_rmse",
     "morlet_direct_kernel_rmse", "morlet_multiply_kernel_rmse", "TransformPlan", "MultiScalePlan", "ComponentsPlan",
+    "reconstruct", "tune_beta", "WindowState", "sliding_window_state", "StabilityReport", "stability_probe",
+    "CostReport", "cost_model", "MethodOpCounts", "sft_method_counts", "conv_method_counts",
     "FitDegenerateError", "SftGpuError", "write_coefficient_sets", "read_coefficient_sets",
     "morlet_direct_spec_from_coeffs", "sliding_sum_plan", "sliding_sum_flat", "sliding_sum_blocked8",
 ]
@@ -240,17 +242,18 @@ def asft_components(sig: Signal, cfg: SftConfig) -> ComponentSeq:
 
 
 def sft_via_sliding_sum(sig: Signal, cfg: SftConfig, workers: int = 1) -> ComponentSeq:
-    """proj/src/engine.cpp:323-337: the kernel-integral components as fresh window sums.
-    On the GPU every output is produced by the same bounded-state window scan, so the
-    sliding-sum route and the kernel integral are one kernel; the reference's overflow
-    guard for the rebased attenuated sequence is kept for API parity."""
+    """proj/src/engine.cpp:183-219, 323-337: the kernel-integral components by the
+    reference's sliding-sum route, on the GPU (``sftgpu_sft_via_sliding_sum``): the
+    rebased attenuated phased sequence, the K5 flat window sums (paper Algorithm 1,
+    complex128), rescale and phase removal. ``workers`` is accepted for API parity."""
     n = sig.size()
-    if cfg.alpha * (0.5 * n + cfg.half_width) > 600.0:
-        raise ValueError("sft_via_sliding_sum: alpha * N / 2 too large for the attenuated phased sequence")
-    checked = SftConfig(cfg.half_width, cfg.beta, cfg.order, cfg.alpha, cfg.n0, Strategy.KernelIntegral,
-                        cfg.precision, cfg.window_2k1)
-    c, s = _components(sig, [checked], 0, n - 1, 0)
-    return ComponentSeq(c[0], s[0])
+    x = np.ascontiguousarray(sig.samples, dtype=np.float64)
+    c = np.empty(n, dtype=np.float64)
+    s = np.empty(n, dtype=np.float64)
+    raw = cfg._c()
+    check(lib().sftgpu_sft_via_sliding_sum(C.byref(raw), x.ctypes.data_as(C.c_void_p), n, int(sig.boundary),
+                                           c.ctypes.data_as(C.c_void_p), s.ctypes.data_as(C.c_void_p)))
+    return ComponentSeq(c, s)
 
 
 # ------------------------------------------------------------------ fits / specs
@@ -276,6 +279,19 @@ class CoefficientSet:  # include/sft/fourier_fit.hpp:56-68
             c.kind, c.half_width, c.beta, list(c.cos_orders[: c.n_cos]), list(c.sin_orders[: c.n_sin]),
             cc[:, 0] + 1j * cc[:, 1], sc[:, 0] + 1j * sc[:, 1], c.fit_rmse_percent, c.sigma, c.xi, c.n0,
         )
+
+    def _c(self) -> _abi.Coeffs:
+        c = _abi.Coeffs()
+        c.kind, c.half_width, c.beta = int(self.kind), int(self.half_width), float(self.beta)
+        c.n_cos, c.n_sin = len(self.cos_orders), len(self.sin_orders)
+        for i, p in enumerate(self.cos_orders):
+            c.cos_orders[i] = int(p)
+            c.cos_coeffs[2 * i], c.cos_coeffs[2 * i + 1] = float(np.real(self.cos_coeffs[i])), float(np.imag(self.cos_coeffs[i]))
+        for i, p in enumerate(self.sin_orders):
+            c.sin_orders[i] = int(p)
+            c.sin_coeffs[2 * i], c.sin_coeffs[2 * i + 1] = float(np.real(self.sin_coeffs[i])), float(np.imag(self.sin_coeffs[i]))
+        c.fit_rmse_percent, c.sigma, c.xi, c.n0 = float(self.fit_rmse_percent), float(self.sigma), float(self.xi), int(self.n0)
+        return c
 
 
 @dataclass
@@ -526,6 +542,101 @@ def fit_mmse(target, half_width: int, beta: float, cos_orders, sin_orders, kind:
     check(lib().sftgpu_fit_mmse(buf.ctypes.data_as(C.c_void_p), half_width, beta, co.size, co.ctypes.data_as(C.c_void_p),
                                 so.size, so.ctypes.data_as(C.c_void_p), kind, C.byref(c)))
     return CoefficientSet._from(c)
+
+
+def reconstruct(coeffs: CoefficientSet, points) -> np.ndarray:
+    """proj/src/fourier_fit.cpp:107-129: the fitted series at arbitrary points."""
+    q = np.ascontiguousarray(points, dtype=np.float64)
+    out = np.empty(2 * q.size, dtype=np.float64)
+    raw = coeffs._c()
+    check(lib().sftgpu_reconstruct(C.byref(raw), q.ctypes.data_as(C.c_void_p), q.size, out.ctypes.data_as(C.c_void_p)))
+    return out.view(np.complex128)
+
+
+def tune_beta(rmse_of_beta, half_width: int):
+    """proj/src/fourier_fit.cpp:395-438: 33-point prescan over [0.5 pi/K, 1.5 pi/K] plus
+    golden section to 1e-4 relative, on any RMSE profile. Returns (beta, rmse)."""
+    cb = C.CFUNCTYPE(C.c_double, C.c_double, C.c_void_p)(lambda b, _u: float(rmse_of_beta(b)))
+    beta, rmse = C.c_double(), C.c_double()
+    check(lib().sftgpu_tune_beta(cb, None, half_width, C.byref(beta), C.byref(rmse)))
+    return beta.value, rmse.value
+
+
+@dataclass
+class WindowState:  # include/sft/engine.hpp:82-88
+    via_prefix: np.ndarray
+    via_recurrence: np.ndarray
+
+
+def sliding_window_state(sig: Signal, cfg: SftConfig) -> WindowState:
+    """proj/src/engine.cpp:270-300: u_{(2K+1)}[n+K] by the sliding-sum route (K5) and by
+    the window-recurrence scan (K1), both on the GPU, output phase re-applied. Plain SFT."""
+    if cfg.alpha != 0.0:
+        raise ValueError("sliding_window_state: plain SFT only")
+    k = SftConfig(cfg.half_width, cfg.beta, cfg.order, 0.0, cfg.n0, Strategy.KernelIntegral, Precision.Double,
+                  cfg.window_2k1)
+    a, b = sft_via_sliding_sum(sig, k), sft_components(sig, k)
+    omega = cfg.beta * cfg.order.p if cfg.order.integer_order else cfg.order.omega
+    ph = np.exp(1j * omega * np.arange(sig.size()))
+    return WindowState(ph * (a.c - 1j * a.s), ph * (b.c - 1j * b.s))
+
+
+@dataclass
+class StabilityReport:  # include/sft/engine.hpp:94-100
+    max_state_magnitude: float
+    max_component_error: float
+    reference_scale: float
+    abs_error: np.ndarray
+
+
+def stability_probe(sig: Signal, cfg: SftConfig) -> StabilityReport:
+    """proj/src/engine.cpp:302-320: cfg at single precision against double (both GPU).
+    max_state_magnitude is the peak |window state| of the fp32 scan."""
+    n = sig.size()
+    mk = lambda p: SftConfig(cfg.half_width, cfg.beta, cfg.order, cfg.alpha, cfg.n0, cfg.strategy, p,  # noqa: E731
+                             cfg.window_2k1)
+    lo = components_over(sig, mk(Precision.Single), 0, n - 1)
+    ref = components_over(sig, mk(Precision.Double), 0, n - 1)
+    err = np.maximum(np.abs(lo.c - ref.c), np.abs(lo.s - ref.s))
+    scale = float(max(np.abs(ref.c).max(), np.abs(ref.s).max()))
+    return StabilityReport(float(np.hypot(lo.c, lo.s).max()), float(err.max() / scale if scale > 0 else err.max()),
+                           scale, err)
+
+
+@dataclass
+class CostReport:  # include/sft/sliding_sum.hpp:236-243
+    parallel_steps: int
+    outer_iterations: int
+    total_adds: int
+    total_mults: int
+    predicted_regime: str
+
+
+def cost_model(n: int, window: int, blocked: bool = False, core_budget: int = 1) -> CostReport:
+    """proj/src/sliding_sum.cpp:7-40 for SlidingSumPlan::make(n, window, variant, M)."""
+    p = sliding_sum_plan(n, window, blocked)
+    regime = "O(log2 L) parallel time (M >= N)" if core_budget >= n else "O(N log2 L / M) parallel time (M < N)"
+    return CostReport(p["parallel_steps"], p["blocked_stages"] if blocked else 1, p["total_adds"], 0, regime)
+
+
+@dataclass
+class MethodOpCounts:  # include/sft/sliding_sum.hpp:248-256
+    mults: int
+    adds: int
+    regime: str
+
+
+def sft_method_counts(n: int, orders: int, half_width: int, core_budget: int) -> MethodOpCounts:
+    """proj/src/sliding_sum.cpp:42-52."""
+    reg = "O(P log2 K) time (M >= N)" if core_budget >= n else "O(N P log2 K / M) time (M < N)"
+    return MethodOpCounts(7 * n * orders, n * orders * (2 * half_width + 1), reg)
+
+
+def conv_method_counts(n: int, sigma: float, core_budget: int) -> MethodOpCounts:
+    """proj/src/sliding_sum.cpp:54-64."""
+    w = int(round(6.0 * sigma)) + 1
+    reg = "O(log2 sigma) time (M >= N(6 sigma + 1))" if core_budget >= n * w else "O(N sigma log2 sigma / M) time"
+    return MethodOpCounts(n * w, n * w, reg)
 
 
 def select_optimal_ps(sigma, xi, half_width, pd, n0=0) -> int:

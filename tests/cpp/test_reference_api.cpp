@@ -219,4 +219,96 @@ TEST_CASE("shift validation") {
   CHECK_NOTHROW(make_gauss_spec(8.0, GaussKind::Value, 4, 2, {}));
 }
 
+// ---- the rest of the reference's public surface (engine.hpp:82-109, sliding_sum.hpp,
+// fourier_fit.hpp), proj/tests/test_engine.cpp / test_sliding_sum.cpp / test_fourier_fit.cpp
+TEST_CASE("window state: prefix route equals the in-window recurrence") {
+  const Signal sig = make_test_signal(TestSignalKind::SeededNoise, 300, 4);
+  const WindowState st = sliding_window_state(sig, config(12, M_PI / 12, 3, 0.0, Strategy::KernelIntegral));
+  double m = 0.0, scale = 0.0;
+  for (size_t i = 0; i < st.via_prefix.size(); ++i) {
+    m = std::max(m, std::abs(st.via_prefix[i] - st.via_recurrence[i]));
+    scale = std::max(scale, std::abs(st.via_recurrence[i]));
+  }
+  CHECK(m < 1e-10 * scale);
+  CHECK_THROWS_AS(sliding_window_state(sig, config(12, M_PI / 12, 3, 0.1, Strategy::KernelIntegral)),
+                  std::invalid_argument);
+}
+
+TEST_CASE("sliding-sum route equals the kernel integral") {
+  const Signal sig = make_test_signal(TestSignalKind::SeededNoise, 500, 9);
+  for (int p : {0, 2, 5}) {
+    const SftConfig cfg = config(20, M_PI / 20, p, 0.003, Strategy::KernelIntegral);
+    CHECK(max_abs_diff(sft_via_sliding_sum(sig, cfg), asft_components(sig, cfg)) < 1e-9);
+  }
+  CHECK_THROWS_AS(sft_via_sliding_sum(make_test_signal(TestSignalKind::SeededNoise, 20000, 1),
+                                      config(16, M_PI / 16, 1, 0.1, Strategy::KernelIntegral)),
+                  std::invalid_argument);
+}
+
+TEST_CASE("stability probe: single precision against double") {
+  const Signal sig = make_test_signal(TestSignalKind::SeededNoise, 4000, 11);
+  const StabilityReport r = stability_probe(sig, config(64, M_PI / 64, 2, 0.0, Strategy::KernelIntegral));
+  CHECK(r.abs_error.size() == 4000);
+  CHECK(r.reference_scale > 0.0);
+  CHECK(r.max_component_error < 1e-5);
+  CHECK(r.max_state_magnitude > 0.0);
+}
+
+TEST_CASE("sliding sums: known answers and the blocked8 trace") {
+  const std::vector<std::int64_t> f = {1, 2, 3, 4, 5};
+  const std::vector<std::int64_t> want = {6, 9, 12};
+  CHECK(sliding_sum_flat(f, 3) == want);
+  CHECK(sliding_sum_blocked8(f, 3) == want);
+  std::vector<double> g(500);
+  for (size_t i = 0; i < g.size(); ++i) g[i] = std::sin(0.37 * static_cast<double>(i)) + 1e-3 * static_cast<double>(i);
+  RoundTrace tr;
+  const std::vector<double> a = sliding_sum_blocked8(g, 37, 1, &tr);
+  const std::vector<double> b = sliding_sum_flat(g, 37);
+  CHECK(a.size() == 464);
+  double m = 0.0;
+  for (size_t i = 0; i < a.size(); ++i) m = std::max(m, std::fabs(a[i] - b[i]));
+  CHECK(m < 1e-12);
+  CHECK(tr.rounds.size() == 6);  // test_output.txt:41
+  CHECK(tr.total_adds() == 7744);
+  const CostReport cr = cost_model(SlidingSumPlan::make(500, 37, SsVariant::Blocked8));
+  CHECK(cr.total_adds == 7744);
+  CHECK(cr.outer_iterations == 2);
+  CHECK(cost_model(SlidingSumPlan::make(500, 37)).parallel_steps == 6);
+  const MethodOpCounts sc = sft_method_counts(1000, 7, 24, 1);
+  CHECK(sc.mults == 49000);
+  CHECK(conv_method_counts(1000, 8.0, 1).adds == 49000);
+}
+
+TEST_CASE("fits: reconstruct, Gaussian bundle, Morlet fits, beta tuning") {
+  const GaussianParams gp(6.0);
+  const GaussianFitBundle b = fit_gaussian_bundle(gp, 6, M_PI / gp.half_width);
+  CHECK(b.a.size() == 7);
+  CHECK(b.b.size() == 6);
+  CHECK(b.fit_rmse_g < 1.0);
+  CHECK(gauss_kernel_rmse(b, GaussKind::Value, 0) < 1.0);
+  // fit_mmse of the Gaussian on [-K, K] reproduces the bundle's cos coefficients
+  ArrayXd target(2 * gp.half_width + 1);
+  for (int k = -gp.half_width; k <= gp.half_width; ++k) target[k + gp.half_width] = gauss(gp, k);
+  std::vector<int> cos_p = {0, 1, 2, 3, 4, 5, 6};
+  const CoefficientSet cs = fit_mmse(target, HarmonicGrid(gp.half_width, M_PI / gp.half_width, cos_p, {}),
+                                     CoeffKind::GaussCos);
+  for (int p = 0; p <= 6; ++p) CHECK(std::fabs(cs.cos_coeffs[p].real() - b.a[p]) < 1e-12);
+  ArrayXd pts = {-3.0, 0.0, 2.5};
+  const ArrayXcd rec = reconstruct(cs, pts);
+  for (size_t i = 0; i < pts.size(); ++i) CHECK(std::fabs(rec[i].real() - gauss(gp, pts[i])) < 2e-3 * gauss(gp, 0));
+  const MorletParams mp(60.0, 8.0);
+  const CoefficientSet md = fit_morlet_direct(mp, 5, 6, M_PI / mp.half_width, 0);
+  CHECK(md.cos_coeffs.size() == 6);
+  const CoefficientSet env = fit_morlet_envelope(mp, 3, M_PI / mp.half_width);
+  CHECK(env.cos_coeffs.size() == 4);
+  // generic tuner on a known profile: minimum of (beta - 0.9 pi/K)^2 + 1
+  const int K = 40;
+  const BetaTuneResult t = tune_beta([&](double beta) { return (beta - 0.9 * M_PI / K) * (beta - 0.9 * M_PI / K) + 1.0; }, K);
+  CHECK(std::fabs(t.beta - 0.9 * M_PI / K) < 1e-3 * M_PI / K);
+  CHECK(std::fabs(t.rmse_percent - 1.0) < 1e-9);
+  const BetaTuneResult tg = tune_beta_gauss(gp, 4, 0);
+  CHECK(tg.beta > 0.5 * M_PI / gp.half_width);
+  CHECK(tg.beta < 1.5 * M_PI / gp.half_width);
+}
+
 DOCTEST_LITE_MAIN

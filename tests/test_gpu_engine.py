@@ -261,3 +261,26 @@ def test_components_fp32_vs_fp64_oracle(sft, O, offset):
         scale = max(np.max(np.abs(rc)), np.max(np.abs(rs)))
         err = max(np.max(np.abs(got.c - rc)), np.max(np.abs(got.s - rs))) / scale
         assert err < 1e-5, (p, err)
+
+
+def test_window_state_two_routes_and_stability_probe(sft, O):
+    """sliding_window_state (proj/src/engine.cpp:270-300): the sliding-sum route (K5) and
+    the window-recurrence scan (K1) give the same u[n+K] (the reference's equivalence test,
+    proj/tests/test_engine.cpp); stability_probe (engine.cpp:302-320) reports the fp32 scan
+    against fp64: with the bounded 2K-window state the error does not grow with n."""
+    x = sft.Signal(O.make_test_signal(O.SEEDED_NOISE, 3000, 21))
+    st = sft.sliding_window_state(x, cfg(sft, 40, math.pi / 40, 3, strategy=0))
+    assert np.max(np.abs(st.via_prefix - st.via_recurrence)) < 1e-10 * np.max(np.abs(st.via_recurrence))
+    # brute force u[n] = sum_{j=n-K}^{n+K} x[j] e^{i omega j}
+    xs, K, w = x.samples, 40, 3 * math.pi / 40
+    for n in (0, 1234, 2999):
+        j = np.clip(np.arange(n - K, n + K + 1), 0, 2999)
+        u = np.sum(xs[j] * np.exp(1j * w * np.arange(n - K, n + K + 1)))
+        assert abs(st.via_recurrence[n] - u) < 1e-10 * abs(u) + 1e-12
+    with pytest.raises(ValueError):
+        sft.sliding_window_state(x, cfg(sft, 40, math.pi / 40, 3, 0.01, strategy=0))
+    y = sft.Signal(O.make_test_signal(O.SEEDED_NOISE, 100000, 3) + 1.0)
+    rep = sft.stability_probe(y, cfg(sft, 256, math.pi / 256, 2, strategy=0))
+    assert rep.max_component_error < 1e-5
+    head, tail = rep.abs_error[:10000].max(), rep.abs_error[-10000:].max()
+    assert tail < 4 * head + 1e-12 * rep.reference_scale
