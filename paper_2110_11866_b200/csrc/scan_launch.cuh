@@ -29,6 +29,12 @@ struct LaunchKey {
   int nord, gm, mode, seq;
 };
 
+// Forward-progress assumption of the LB (look-back) launches: tile = blockIdx.x and a tile
+// waits only on lower tiles, so progress relies on blocks being dispatched in index order
+// with every earlier block already resident or finished (the assumption CUB's single-pass
+// scan makes too). A plan's LB launches are serialised (sftgpu_api.cu, lb_order_begin);
+// running LB plans concurrently with other kernels that occupy every SM (e.g. under MPS)
+// can delay lower tiles but not deadlock as long as started blocks run to completion.
 template <typename T, int MODE, bool SEQ>
 void launch_scan(const LaunchKey& key, const ScanParams<T>& p, long long grid, cudaStream_t s);
 
