@@ -51,7 +51,7 @@ namespace tck {
 
 struct Misc {
   uint64_t xfull[2], xfree[2], g1done[2], dfree[2], sready[2], g2done[2];
-  uint64_t fullL[kLoadAhead + 1], fullT[kLoadAhead + 1];  // loader ring slots landed (lead, trail)
+  uint64_t fullL[kLoadAhead + 1], fullT[kTrailAhead + 1];  // loader ring slots landed (lead, trail)
   uint64_t drain, scandone, imgbar;  // scale switch: MMAs done, scans done, new image landed
   uint32_t tmem;
   double2 cy[2][kMaxOrd];  // tile carry (state entering the tile), fp64, by tile parity
@@ -185,7 +185,7 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
 enum StreamKind { kTma = 0, kCp = 1, kZero = 2, kFirst = 3, kLast = 4, kMixed = 5 };
 __device__ __forceinline__ int stream_kind(const TcParams& P, long long a, long long j0, long long jmin, bool lead) {
   if (P.use_tma_in && a >= 0 && a >= jmin && a + kBoxRows * 32 <= P.n) {
-    if (lead && (a >> 5) + kBoxRows <= P.in_rows) return kTma;
+    if ((lead || TCK_TRAIL_TMA) && (a >> 5) + kBoxRows <= P.in_rows) return kTma;
     return kCp;
   }
   const long long j1 = j0 + kTile;
@@ -374,10 +374,8 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     umma::mbar_init(&M.drain, 1);
     umma::mbar_init(&M.scandone, 256);
     umma::mbar_init(&M.imgbar, 1);
-    for (int k = 0; k <= kLoadAhead; ++k) {
-      umma::mbar_init(&M.fullL[k], 129);  // TMA issuer + 128 cp.async arrivals
-      umma::mbar_init(&M.fullT[k], 128);
-    }
+    for (int k = 0; k <= kLoadAhead; ++k) umma::mbar_init(&M.fullL[k], 129);  // TMA issuer + 128 cp.async arrivals
+    for (int k = 0; k <= kTrailAhead; ++k) umma::mbar_init(&M.fullT[k], TCK_TRAIL_TMA ? 129 : 128);
     umma::mbar_fence_init();
   }
   __syncthreads();  // image (g0) in shared memory
@@ -500,9 +498,9 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
   } else if (warp >= 12) {
     // ================= loader: two groups of four warps, one per stream (warps 12-15 the
     // lead, 16-19 the trail); in each, thread t = chunk row t = TMEM lane t (warp w: lanes
-    // [32 (w % 4), +32)). Each group stages its stream kLoadAhead tiles ahead into its
-    // ring (the lead by TMA, the trail and boundary segments by cp.async), then moves its
-    // rows into the X operand in TMEM.
+    // [32 (w % 4), +32)). Each group stages its stream `ahead` tiles ahead into its ring
+    // (TMA boxes inside the signal, boundary segments by cp.async), then moves its rows into
+    // the X operand in TMEM.
     const bool lead = warp < 16;
     const int t = tid - (lead ? 384 : 512);
     const uint32_t lrow = static_cast<uint32_t>((warp & 3) * 32) << 16;
@@ -510,9 +508,14 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     unsigned char* const ring = sm + (lead ? kLStage : kTrail);
     const uint32_t stride = lead ? kLeadBytes : kTrailBytes;
     uint64_t* const full = lead ? M.fullL : M.fullT;
-    unsigned long long keep;  // lead lines are read again 2K positions later as the trail
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+    // lead lines are read again 2K positions later as the trail, which is their last use
+    unsigned long long keep;
+    if (lead)
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+    else
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(keep));
     if (P.dbg & 2) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(keep));
+    const int ahead = lead ? kLoadAhead : kTrailAhead;
     // this group's stream of a tile: x[n + K] (lead) or x[n - K] (trail) from n = lo + o0,
     // its start rounded down to 16 bytes (r samples before the first one used), its kind
     auto stream = [&](const Walk& w, long long& a, long long& jmin, int& r) {
@@ -525,17 +528,17 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       if (!lead && w.warm(P)) return static_cast<int>(kZero);  // warm tiles: no trail operand
       return stream_kind(P, a, a + r, jmin, lead);
     };
-    // stage tile w into ring slot `slot`: a lead box by TMA (one thread, transaction bytes
-    // on fullL[slot]), everything else by cp.async from the group's 128 threads, each of
-    // which then arrives on the slot's barrier once its copies have landed
+    // stage tile w into ring slot `slot`: a box by TMA (one thread, transaction bytes on
+    // full[slot]), everything else by cp.async from the group's 128 threads, each of which
+    // then arrives on the slot's barrier once its copies have landed
     auto issue = [&](const Walk& w, int slot, long long gtrace) {
       if (!w.valid) return;
       long long a, jmin;
       int r;
       const int k = stream(w, a, jmin, r);
       unsigned char* const sl = ring + slot * stride;
-      if (lead && t == 0) {
-        trace_ev(P, gtrace, 13);
+      if ((lead || TCK_TRAIL_TMA) && t == 0) {
+        if (lead) trace_ev(P, gtrace, 13);
         umma::mbar_arrive_tx(&full[slot], k == kTma ? kBoxBytes : 0u);
         if (k == kTma)
           umma::tma_load_3d(umma::smem_u32(sl), &P.in_map, &full[slot], static_cast<int>(a & 31),
@@ -544,28 +547,28 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       if (k != kTma) stage_stream(P, P.x + w.sig * P.ld_x, a, jmin, k, t, sl);
       cp_async_arrive(&full[slot]);
     };
-    // ring of kLoadAhead + 1 tiles: tile gt + kLoadAhead is issued before tile gt is moved
-    // into TMEM (its slot was last read by tile gt - 1, before the group's barrier)
+    // ring of ahead + 1 tiles: tile gt + ahead is issued before tile gt is moved into TMEM
+    // (its slot was last read by tile gt - 1, before the group's barrier)
     uint32_t fph = 0;  // full[] phase bits
     Walk wi, w;
     wi.begin(P);
     w.begin(P);
-    for (int k = 0; k < kLoadAhead; ++k) {
+    for (int k = 0; k < ahead; ++k) {
       issue(wi, k, k);
       if (wi.valid) wi.advance(P);
     }
+    int slot = 0, islot = ahead;  // ring slots of tile gt and of tile gt + ahead
     for (long long gt = 0; w.valid; ++gt) {
-      issue(wi, static_cast<int>((gt + kLoadAhead) % (kLoadAhead + 1)), gt + kLoadAhead);
+      issue(wi, islot, gt + ahead);
       if (wi.valid) wi.advance(P);
-      if (lead && t == 0) trace_ev(P, gt, 11);
-      const int slot = static_cast<int>(gt % (kLoadAhead + 1));
+      if (!lead && t == 0) trace_ev(P, gt + ahead, 11);  // trail tile gt + ahead issued
       long long a, jmin;
       int r;
       const int k = stream(w, a, jmin, r);
       umma::mbar_wait(&full[slot], (fph >> slot) & 1u);
       fph ^= 1u << slot;
       umma::fence_proxy_async();  // the cp.async writes precede a later TMA box in this slot
-      if (lead && t == 0) trace_ev(P, gt, 10);
+      if (t == 0) trace_ev(P, gt, lead ? 10 : 15);  // slot landed (lead / trail group)
       const int b = static_cast<int>(gt & 1);
       if (gt >= 2) umma::mbar_wait(&M.xfree[b], static_cast<uint32_t>(((gt >> 1) - 1) & 1));
       __syncwarp();
@@ -581,12 +584,14 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
         row_to_tmem(sl, r, t, tx);
       else if (lead || !w.warm(P))  // uniform: zero, x[0] (kFirst) or x[n - 1] (kLast)
         uniform_to_tmem(k == kZero ? 0.f : *reinterpret_cast<const float*>(sl + kValOff + (k == kLast ? 4 : 0)), tx);
-      if (lead && t == 0) trace_ev(P, gt, 12);
+      if (!lead && t == 0) trace_ev(P, gt, 12);  // trail group: rows written
       umma::tmem_wait_st();
       umma::fence_before();
       umma::mbar_arrive(&M.xfull[b]);
       bar_named(bar_id, 128);  // every row of the slot has been read: it may be refilled
       w.advance(P);
+      slot = slot == ahead ? 0 : slot + 1;
+      islot = islot == ahead ? 0 : islot + 1;
     }
   } else if (warp >= 8) {
     // ================= epilogue (non-warm tiles): thread = chunk = TMEM lane

@@ -25,19 +25,31 @@ constexpr uint32_t kZ128 = 49152;   // float2 [kMaxOrd][32]: z^{128 t}
 constexpr uint32_t kZs = 51200;     // float2 [kMaxOrd][8]: z^{32}, z^{128 * 2^k} (k < 5)
 constexpr uint32_t kZd = 51712;     // double2 [3][kMaxOrd]: z^{4096}, (unused), g0
 constexpr uint32_t kImage = 52096;  // bytes copied from the plan's device image
-// Loader staging: a ring of kLoadAhead + 1 tiles. Each tile stream is 129 SW128 rows of
-// 32 samples (row rho, column i = sample a + 32 rho + i, a = the stream's first sample
-// rounded down to 16 bytes; the 129th row carries the <= 3 samples a misaligned stream
-// spills past 4096), followed by one word for a uniform stream's value. Lead streams are
-// TMA boxes (1024-aligned destinations); trail streams are cp.async'd (128-aligned).
-constexpr int kLoadAhead = 3;                    // tiles in flight ahead of the one moved to TMEM
+// Loader staging: one ring per stream, kLoadAhead + 1 (lead) / kTrailAhead + 1 (trail)
+// tiles. Each tile stream is 129 SW128 rows of 32 samples (row rho, column i = sample
+// a + 32 rho + i, a = the stream's first sample rounded down to 16 bytes; the 129th row
+// carries the <= 3 samples a misaligned stream spills past 4096), followed by one word for a
+// uniform stream's value. Both streams are TMA boxes inside the signal (1024-aligned
+// destinations); the trail reads lines the lead brought into L2 2K samples earlier, so it
+// runs fewer tiles ahead. TCK_TRAIL_TMA=0 restores the round-2 16-byte cp.async trail.
+#ifndef TCK_TRAIL_TMA
+#define TCK_TRAIL_TMA 1
+#endif
+#ifndef TCK_LEAD_AHEAD
+#define TCK_LEAD_AHEAD 3
+#endif
+#ifndef TCK_TRAIL_AHEAD
+#define TCK_TRAIL_AHEAD (TCK_TRAIL_TMA ? 2 : 3)
+#endif
+constexpr int kLoadAhead = TCK_LEAD_AHEAD;       // lead tiles in flight ahead of the one moved to TMEM
+constexpr int kTrailAhead = TCK_TRAIL_AHEAD;     // trail tiles in flight
 constexpr uint32_t kBoxRows = kNC + 1;           // 129 rows per stream
-constexpr uint32_t kBoxBytes = kBoxRows * 128;   // 16512 bytes of TMA transaction per lead box
+constexpr uint32_t kBoxBytes = kBoxRows * 128;   // 16512 bytes of TMA transaction per box
 constexpr uint32_t kLeadBytes = 17408;           // lead stride (1024-aligned)
-constexpr uint32_t kTrailBytes = 16640;          // trail stride (rows + value word, 128-aligned)
+constexpr uint32_t kTrailBytes = TCK_TRAIL_TMA ? 17408 : 16640;  // trail stride (1024- / 128-aligned)
 constexpr uint32_t kLStage = (kImage + 1023) / 1024 * 1024;                 // lead ring
 constexpr uint32_t kTrail = kLStage + (kLoadAhead + 1) * kLeadBytes;       // trail ring
-constexpr uint32_t kStage = kTrail + (kLoadAhead + 1) * kTrailBytes;       // epilogue staging (SW128)
+constexpr uint32_t kStage = kTrail + (kTrailAhead + 1) * kTrailBytes;       // epilogue staging (SW128)
 constexpr uint32_t kScr = kStage + 32768;  // epilogue staging: two halves; then the scan's
                                            // aggregates / states [order][chunk] (aliased)
 constexpr uint32_t kMisc = kScr + kMaxOrd * kNC * 8;

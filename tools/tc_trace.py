@@ -30,7 +30,7 @@ torch.cuda.synchronize()
 lib.sftgpu_debug_set_tc_trace(None)
 t = tr.cpu().numpy().reshape(64, 16).astype(np.int64)
 t0 = t[t > 0].min()
-names = ["ld_go", "mma_go", "g1_iss", "scan_g1", "st_tmem", "g2_iss", "epi_g2", "epi_end", "ph1", "ph2", "ld_full", "iss_done", "lead_rd", "tma_iss", "e_rel", "rd_start"]
+names = ["ld_go", "mma_go", "g1_iss", "scan_g1", "st_tmem", "g2_iss", "epi_g2", "epi_end", "ph1", "ph2", "ld_full", "trail_iss", "trail_done", "tma_iss", "e_rel", "trail_full"]
 print("tile " + " ".join(f"{n:>8s}" for n in names))
 for g in range(64):
     print(f"{g:4d} " + " ".join(f"{(v - t0) if v > 0 else -1:8d}" for v in t[g]))
