@@ -55,6 +55,7 @@ struct Misc {
   uint64_t drain, scandone, imgbar;  // scale switch: MMAs done, scans done, new image landed
   uint32_t tmem;
   double2 cy[2][kMaxOrd];  // tile carry (state entering the tile), fp64, by tile parity
+  float2 tot[kMaxOrd];     // tile total of the order's chunk scan (lane 31 of phase 2)
 };
 static_assert(sizeof(Misc) <= 512, "Misc region");
 
@@ -152,6 +153,9 @@ __device__ __forceinline__ double2 seg_carry(const TcParams& P, const Walk& w, i
 // -DTCK_TRACE=1 (SFTGPU_EXTRA_NVCC_FLAGS): the checks cost issue slots in every role.
 #ifndef TCK_TRACE
 #define TCK_TRACE 0
+#endif
+#ifndef TCK_SCANPROBE
+#define TCK_SCANPROBE 0
 #endif
 __device__ __forceinline__ void trace_ev(const TcParams& P, long long gt, int ev) {
   if constexpr (TCK_TRACE) {
@@ -331,6 +335,13 @@ __device__ __forceinline__ void merged_k(uint64_t db, uint32_t d, uint32_t x, ui
   umma::mma_tf32_ts<kBTh + ko>(d, x + 96 + 8 * K, db, id, 1);       // xt_l . BT_h
   umma::mma_tf32_ts<kBTl + ko>(d, x + 64 + 8 * K, db, id, 1);       // xt_h . BT_l
 }
+// timing probe (dbg 32): the hi . hi products only (wrong results)
+template <int K>
+__device__ __forceinline__ void merged_hh(uint64_t db, uint32_t d, uint32_t x, uint32_t id) {
+  constexpr uint32_t ko = 32 * K;
+  umma::mma_tf32_ts<kBLh + ko>(d, x + 8 * K, db, id, K > 0);
+  umma::mma_tf32_ts<kBTh + ko>(d, x + 64 + 8 * K, db, id, 1);
+}
 // Warm-up tile: aggregates only (lead stream; the trail is before the warm start)
 template <int K, uint32_t NO>
 __device__ __forceinline__ void warm_k(uint64_t db, uint32_t d, uint32_t x, uint32_t id) {
@@ -466,13 +477,21 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
             if (lane == 0) trace_ev(P, gt - 1, 5);
           }
         };
-        merged_k<0>(dbase, d, x, idm);
-        poll();
-        merged_k<1>(dbase, d, x, idm);
-        poll();
-        merged_k<2>(dbase, d, x, idm);
-        poll();
-        merged_k<3>(dbase, d, x, idm);
+        if (P.dbg & 32) {
+          merged_hh<0>(dbase, d, x, idm);
+          merged_hh<1>(dbase, d, x, idm);
+          poll();
+          merged_hh<2>(dbase, d, x, idm);
+          merged_hh<3>(dbase, d, x, idm);
+        } else {
+          merged_k<0>(dbase, d, x, idm);
+          poll();
+          merged_k<1>(dbase, d, x, idm);
+          poll();
+          merged_k<2>(dbase, d, x, idm);
+          poll();
+          merged_k<3>(dbase, d, x, idm);
+        }
       } else if (NO == 64) {
         warm_k<0, 64>(dbase, d + 64, x, ida);
         warm_k<1, 64>(dbase, d + 64, x, ida);
@@ -538,9 +557,10 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       const int k = stream(w, a, jmin, r);
       unsigned char* const sl = ring + slot * stride;
       if ((lead || TCK_TRAIL_TMA) && t == 0) {
-        if (lead) trace_ev(P, gtrace, 13);
-        umma::mbar_arrive_tx(&full[slot], k == kTma ? kBoxBytes : 0u);
-        if (k == kTma)
+        if (lead && !TCK_SCANPROBE) trace_ev(P, gtrace, 13);
+        const bool box = k == kTma && !(P.dbg & 8);  // dbg 8: timing probe without input boxes
+        umma::mbar_arrive_tx(&full[slot], box ? kBoxBytes : 0u);
+        if (box)
           umma::tma_load_3d(umma::smem_u32(sl), &P.in_map, &full[slot], static_cast<int>(a & 31),
                             static_cast<int>(a >> 5), w.sig, keep);
       }
@@ -561,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
     for (long long gt = 0; w.valid; ++gt) {
       issue(wi, islot, gt + ahead);
       if (wi.valid) wi.advance(P);
-      if (!lead && t == 0) trace_ev(P, gt + ahead, 11);  // trail tile gt + ahead issued
+      if (!lead && t == 0 && !TCK_SCANPROBE) trace_ev(P, gt + ahead, 11);  // trail tile gt + ahead issued
       long long a, jmin;
       int r;
       const int k = stream(w, a, jmin, r);
@@ -584,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
         row_to_tmem(sl, r, t, tx);
       else if (lead || !w.warm(P))  // uniform: zero, x[0] (kFirst) or x[n - 1] (kLast)
         uniform_to_tmem(k == kZero ? 0.f : *reinterpret_cast<const float*>(sl + kValOff + (k == kLast ? 4 : 0)), tx);
-      if (!lead && t == 0) trace_ev(P, gt, 12);  // trail group: rows written
+      if (!lead && t == 0 && !TCK_SCANPROBE) trace_ev(P, gt, 12);  // trail group: rows written
       umma::tmem_wait_st();
       umma::fence_before();
       umma::mbar_arrive(&M.xfull[b]);
@@ -644,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
           const int row0 = static_cast<int>((w.obase() + o0) / kQ), sg = w.unit(P);
           unsigned long long spol;
           asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(spol));
-          for (int h = 0; h < halves; ++h) {
+          for (int h = 0; h < ((P.dbg & 16) ? 0 : halves); ++h) {  // dbg 16: timing probe without stores
             const uint32_t src = umma::smem_u32(stgo + h * 16384);
             if (P.cplx && (P.dbg & 4))
               asm volatile(
@@ -740,27 +760,32 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       if (tid == 0) trace_ev(P, gt, 8);
       if (warm && tid == 0) umma::mbar_arrive_cnt(&M.dfree[b], 128);  // nothing else reads it
       if (p < nord) {
-        const float2 z32 = zs[p * 8];
+        float2 zk[6];  // this order's multipliers: z^32, z^{128 2^k} (k < 5)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) zk[k] = zs[p * 8 + k];
+        const float2 zc = z128[p * 32 + lane];
+        const float2 z32 = zk[0];
         const float4 a01 = *reinterpret_cast<const float4*>(At + p * kNC + 4 * lane);
         const float4 a23 = *reinterpret_cast<const float4*>(At + p * kNC + 4 * lane + 2);
         const float2 a0 = make_float2(a01.x, a01.y), a1 = make_float2(a01.z, a01.w);
         const float2 a2 = make_float2(a23.x, a23.y), a3 = make_float2(a23.z, a23.w);
         // group total: sum_j z^{32 (3 - j)} a_j
         float2 g = cmla(z32, cmla(z32, cmla(z32, a0, a1), a2), a3);
+        if (TCK_SCANPROBE && p == 0 && lane == 0) trace_ev(P, gt, 13);
         // inclusive warp scan over groups, multiplier z^{128 2^k}
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
           const int d = 1 << k;
           const float2 tt = make_float2(__shfl_up_sync(0xffffffffu, g.x, d), __shfl_up_sync(0xffffffffu, g.y, d));
-          if (lane >= d) g = cmla(zs[p * 8 + 1 + k], tt, g);
+          if (lane >= d) g = cmla(zk[1 + k], tt, g);
         }
+        if (TCK_SCANPROBE && p == 0 && lane == 0) trace_ev(P, gt, 11);
         // fp64 tile carry C (state entering the tile); state entering chunk 4t:
         // sum of the earlier groups (exclusive scan) + z^{128 t} C
         const double2 C = M.cy[b][p];
         float2 e = make_float2(__shfl_up_sync(0xffffffffu, g.x, 1), __shfl_up_sync(0xffffffffu, g.y, 1));
         if (lane == 0) e = make_float2(0.f, 0.f);
         if (!warm) {
-          const float2 zc = z128[p * 32 + lane];
           const float2 cf = make_float2(static_cast<float>(C.x), static_cast<float>(C.y));
           const float2 cz = cmla(zc, cf, make_float2(0.f, 0.f));
           const float2 s0 = make_float2(e.x + cz.x, e.y + cz.y);
@@ -768,15 +793,7 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
           *reinterpret_cast<float4*>(St + p * kNC + 4 * lane) = make_float4(s0.x, s0.y, s1.x, s1.y);
           *reinterpret_cast<float4*>(St + p * kNC + 4 * lane + 2) = make_float4(s2.x, s2.y, s3.x, s3.y);
         }
-        if (lane == 31) {
-          // carry into the next tile (fp64): z^{4096} C + (tile total)
-          const double2 zt = zd[p];
-          Walk nx = w;
-          if (w.last(P)) nx.advance(P);
-          M.cy[b ^ 1][p] = w.last(P) ? seg_carry(P, nx, p)
-                                     : make_double2(fma(zt.x, C.x, fma(-zt.y, C.y, static_cast<double>(g.x))),
-                                                    fma(zt.x, C.y, fma(zt.y, C.x, static_cast<double>(g.y))));
-        }
+        if (lane == 31) M.tot[p] = g;
       }
       bar_named(5, 256);  // states in shared memory; At / St free for the next tile after phase 3
       if (tid == 0) trace_ev(P, gt, 9);
@@ -805,6 +822,18 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
         umma::mbar_arrive(&M.sready[s]);
         if (tid == 0) trace_ev(P, gt, 4);
         ++u;
+      }
+      // carry into the next tile (fp64): z^{4096} C + (tile total), off the state GEMM's
+      // path (read by the next tile's phase 2, after its phase-1 barrier)
+      if (p < nord && lane == 31) {
+        const double2 zt = zd[p], Cin = M.cy[b][p];
+        const float2 gtot = M.tot[p];
+        Walk nx = w;
+        if (w.last(P)) nx.advance(P);
+        M.cy[b ^ 1][p] = w.last(P) ? seg_carry(P, nx, p)
+                                   : make_double2(fma(zt.x, Cin.x, fma(-zt.y, Cin.y, static_cast<double>(gtot.x))),
+                                                  fma(zt.x, Cin.y, fma(zt.y, Cin.x, static_cast<double>(gtot.y))));
+        if (TCK_SCANPROBE && p == 0) trace_ev(P, gt, 12);
       }
       if (w.last(P)) {
         Walk nx = w;
