@@ -600,7 +600,8 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
         fill_mixed(P.n, P.boundary, umma::smem_u32(sl), t, a, jmin);
         bar_named(bar_id, 128);
       }
-      if (k == kTma || k == kCp || k == kMixed)
+      if (P.dbg & 128) {  // dbg 128: timing probe without the X operand stores
+      } else if (k == kTma || k == kCp || k == kMixed)
         row_to_tmem(sl, r, t, tx);
       else if (lead || !w.warm(P))  // uniform: zero, x[0] (kFirst) or x[n - 1] (kLast)
         uniform_to_tmem(k == kZero ? 0.f : *reinterpret_cast<const float*>(sl + kValOff + (k == kLast ? 4 : 0)), tx);
@@ -636,9 +637,14 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       // tiles on); then registers -> staging (row c: 8 chunks of 16 B per half, chunk q at
       // q ^ (c & 7): the TMA SWIZZLE_128B layout of a [128 rows][32 floats] box)
       uint32_t v[2][32];
-      umma::tmem_ld32(tmem + lrow + dcol, v[0]);
-      if (halves == 2) umma::tmem_ld32(tmem + lrow + dcol + 32, v[1]);
-      umma::tmem_wait_ld();
+      if (!(P.dbg & 64)) {  // dbg 64: timing probe without the accumulator load
+        umma::tmem_ld32(tmem + lrow + dcol, v[0]);
+        if (halves == 2) umma::tmem_ld32(tmem + lrow + dcol + 32, v[1]);
+        umma::tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[0][i] = v[1][i] = static_cast<uint32_t>(c + i);
+      }
       umma::fence_before();
       umma::mbar_arrive(&M.dfree[gt & 1]);
       if (c == 0) trace_ev(P, gt, 14);

@@ -112,7 +112,8 @@ struct TcParams {
   int boundary, nord, cplx, vec_ok, use_tma, use_tma_in;
   long long* trace;  // optional: per-tile event clocks of CTA 0 ([64][16]), tools/tc_trace.py
   int dbg;           // experiment switches (SFTGPU_TC_DBG): 2 no lead L2 hint, 4 evict-first output stores;
-                     // timing probes (wrong results): 8 no input boxes, 16 no output stores, 32 hi.hi MMAs only
+                     // timing probes (wrong results): 8 no input boxes, 16 no output stores, 32 hi.hi MMAs only,
+                     // 64 no accumulator load in the epilogue, 128 no X operand stores by the loaders
 };
 
 cudaError_t launch_tc(const TcParams& p, int grid, cudaStream_t s);
