@@ -164,7 +164,19 @@ ComponentSeq run_components(const Signal& sig, const SftConfig& cfg, std::int64_
   check(sftgpu_components_execute_host(plan.p, x.data(), c.data(), s.data(), nullptr));
   return ComponentSeq{ArrayXd(c.begin(), c.end()), ArrayXd(s.begin(), s.end())};
 }
+// Recursive1/2 (engine.cpp:53-120) replayed on the GPU with the reference's rounding (K7)
+inline ComponentSeq replay(const Signal& sig, const SftConfig& cfg, std::int64_t lo, std::int64_t hi, int mode) {
+  if (mode == 1 && cfg.alpha != 0.0) throw std::invalid_argument("sft_components: alpha must be 0 (use asft_components)");
+  if (mode == 2 && !(cfg.alpha > 0.0)) throw std::invalid_argument("asft_components: alpha must be > 0");
+  const sftgpu_config rc = cfg.raw();
+  const size_t cnt = hi >= lo ? static_cast<size_t>(hi - lo + 1) : 1;
+  ComponentSeq out{ArrayXd(cnt), ArrayXd(cnt)};
+  check(sftgpu_components_replay(&rc, 1, sig.samples.data(), sig.size(), static_cast<int>(sig.boundary), lo, hi,
+                                 out.c.data(), out.s.data()));
+  return out;
+}
 inline ComponentSeq components(const Signal& sig, const SftConfig& cfg, std::int64_t lo, std::int64_t hi, int mode) {
+  if (cfg.strategy != Strategy::KernelIntegral && cfg.order.integer_order) return replay(sig, cfg, lo, hi, mode);
   if (cfg.precision == Precision::Single) return run_components<float>(sig, cfg, lo, hi, mode);
   return run_components<double>(sig, cfg, lo, hi, mode);
 }

@@ -31,6 +31,8 @@
  *   sftgpu_components_execute       components_over / sft_components /
  *                                   asft_components / sft_via_sliding_sum
  *                                                              src/engine.cpp:255-269, :323-337
+ *   sftgpu_components_replay        recursive_components (Recursive1/2 with the
+ *                                   reference's rounding)      src/engine.cpp:53-120
  *   sftgpu_generate_signal          make_test_signal           src/signal.cpp:24-51
  *   sftgpu_truncated_convolution    truncated_convolution      src/kernels.cpp:35-51
  */
@@ -341,6 +343,20 @@ int sftgpu_sliding_sum(int dtype, int blocked, const void* f, int64_t n, int64_t
  * same argument checks as the reference (alpha * N / 2 > 600 rejected). */
 int sftgpu_sft_via_sliding_sum(const sftgpu_config* cfg, const double* x_host, int64_t n, int boundary,
                                double* c_host, double* s_host);
+
+/* The reference's recursive strategies with the reference's own rounding (K7,
+ * src/engine.cpp:53-120 recursive_components, dispatched from :221-243): Recursive1
+ * (v = z v + x) or Recursive2 (the real second-order form), each step in the reference's
+ * operation order without FMA contraction (pass 1, one GPU thread per order, filter states
+ * in HBM), then the 2K or 2K+1 truncation window, the z^{-K} unwind and the sink (pass 2,
+ * parallel). Bit-identical to the reference's components_over for these strategies, in
+ * Single (float arithmetic) and Double. The kernel-integral window recurrence (K1, every
+ * strategy through sftgpu_components_plan_create) is the fast path and the more accurate
+ * one; this entry is for callers who need the reference's numbers exactly.
+ * cfgs: n_orders configs with strategy SFTGPU_RECURSIVE1/2 (any K / alpha / precision mix);
+ * HOST fp64 signal in; c = Re, s = -Im out, [n_orders][hi - lo + 1]; synchronous. */
+int sftgpu_components_replay(const sftgpu_config* cfgs, int n_orders, const double* x_host, int64_t n,
+                             int boundary, int64_t lo, int64_t hi, double* c_host, double* s_host);
 
 /* Host-memory variants (device buffers managed internally; synchronous). */
 int sftgpu_sliding_sum_host(int dtype, int blocked, const void* f_host, int64_t n, int64_t L, void* out_host);

@@ -20,7 +20,7 @@ from ._abi import FitDegenerateError, SftGpuError, check, lib
 
 __all__ = [
     "BoundaryPolicy", "Precision", "Strategy", "TransformKind", "GaussKind", "TestSignalKind",
-    "Signal", "make_test_signal", "generate_signals", "OrderSpec", "SftConfig", "ComponentSeq", "TransformOptions",
+    "Signal", "make_test_signal", "generate_signals", "OrderSpec", "SftConfig", "components_replay", "ComponentSeq", "TransformOptions",
     "TransformSpec", "TransformResult", "KernelTaps", "AbbrevInfo", "GaussianFitBundle",
     "CoefficientSet", "parse_abbreviation", "encode_abbreviation", "make_transform_spec",
     "make_gauss_spec", "make_morlet_direct_spec", "make_morlet_multiply_spec", "gauss_smooth",
@@ -223,22 +223,51 @@ def _components(sig: Signal, cfgs, lo: int, hi: int, mode: int):
     return c.double().cpu().numpy(), s.double().cpu().numpy()
 
 
-def components_over(sig: Signal, cfg: SftConfig, lo: int, hi: int) -> ComponentSeq:
-    """proj/src/engine.cpp:255-258 (signed output range, boundary-extended reads)."""
-    c, s = _components(sig, [cfg], lo, hi, 0)
+def components_replay(sig: Signal, cfgs, lo: int, hi: int):
+    """proj/src/engine.cpp:53-120 (recursive_components): Recursive1 / Recursive2 replayed on
+    the GPU with the reference's own operation order (K7, ``sftgpu_components_replay``), so
+    the result is bit-identical to the reference's. (c, s) as [n_cfgs][hi - lo + 1]."""
+    cfgs = list(cfgs)
+    n = sig.size()
+    count = hi - lo + 1 if hi >= lo else 0
+    x = np.ascontiguousarray(sig.samples, dtype=np.float64)
+    c = np.empty((len(cfgs), max(count, 1)), dtype=np.float64)
+    s = np.empty_like(c)
+    arr = (_abi.Config * len(cfgs))(*[cf._c() for cf in cfgs])
+    check(lib().sftgpu_components_replay(arr, len(cfgs), x.ctypes.data_as(C.c_void_p), n, int(sig.boundary), lo, hi,
+                                         c.ctypes.data_as(C.c_void_p), s.ctypes.data_as(C.c_void_p)))
+    return c, s
+
+
+def _one(sig: Signal, cfg: SftConfig, lo: int, hi: int, mode: int, exact: bool) -> ComponentSeq:
+    # Recursive strategies replay the reference's recurrence (bit-identical) unless the
+    # caller asks for the window-recurrence scan (K1, faster and more accurate)
+    if exact and cfg.strategy != Strategy.KernelIntegral and cfg.order.integer_order:
+        if mode == 1 and cfg.alpha != 0.0:
+            raise ValueError("sft_components: alpha must be 0 (use asft_components)")
+        if mode == 2 and not cfg.alpha > 0.0:
+            raise ValueError("asft_components: alpha must be > 0")
+        c, s = components_replay(sig, [cfg], lo, hi)
+    else:
+        c, s = _components(sig, [cfg], lo, hi, mode)
     return ComponentSeq(c[0], s[0])
 
 
-def sft_components(sig: Signal, cfg: SftConfig) -> ComponentSeq:
+def components_over(sig: Signal, cfg: SftConfig, lo: int, hi: int, exact: bool = True) -> ComponentSeq:
+    """proj/src/engine.cpp:255-258 (signed output range, boundary-extended reads).
+    Recursive1/2 configs run the reference's recurrence on the GPU (K7, bit-identical);
+    ``exact=False`` runs every strategy on the window-recurrence scan (K1)."""
+    return _one(sig, cfg, lo, hi, 0, exact)
+
+
+def sft_components(sig: Signal, cfg: SftConfig, exact: bool = True) -> ComponentSeq:
     """proj/src/engine.cpp:260-264 (requires alpha == 0)."""
-    c, s = _components(sig, [cfg], 0, sig.size() - 1, 1)
-    return ComponentSeq(c[0], s[0])
+    return _one(sig, cfg, 0, sig.size() - 1, 1, exact)
 
 
-def asft_components(sig: Signal, cfg: SftConfig) -> ComponentSeq:
+def asft_components(sig: Signal, cfg: SftConfig, exact: bool = True) -> ComponentSeq:
     """proj/src/engine.cpp:266-269 (requires alpha > 0)."""
-    c, s = _components(sig, [cfg], 0, sig.size() - 1, 2)
-    return ComponentSeq(c[0], s[0])
+    return _one(sig, cfg, 0, sig.size() - 1, 2, exact)
 
 
 def sft_via_sliding_sum(sig: Signal, cfg: SftConfig, workers: int = 1) -> ComponentSeq:
