@@ -23,6 +23,11 @@ lib = _abi.lib()
 lib.sftgpu_debug_set_scan_trace.argtypes = [C.c_void_p]
 for _ in range(20):
     plan.execute(xb, out)
+cold = "cold" in sys.argv  # fresh input/output buffers and 2x L2 written before the traced run
+if cold:
+    xb = xb.clone()
+    out = plan.empty_output()
+    torch.empty(2 * 126 * 2**20 // 4, dtype=torch.int32, device="cuda").fill_(1)
 lib.sftgpu_debug_set_scan_trace(C.c_void_p(tr.data_ptr()))
 plan.execute(xb, out)
 torch.cuda.synchronize()
