@@ -64,11 +64,18 @@ __global__ void recursive_chain_kernel(const RcParams<S>* ps, int n_orders, cons
   if (o >= n_orders) return;
   const RcParams<S> P = ps[o];
   S v1r = 0, v1i = 0, v2r = 0, v2i = 0, px = 0;
-  constexpr int kU = 8;  // samples loaded ahead of the dependent chain
+  // samples are loaded one batch ahead of the dependent chain (software pipeline), so
+  // their latency hides behind the previous batch's kU serial steps
+  constexpr int kU = 16;
+  S nx[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) nx[u] = static_cast<S>(ext(x, n, boundary, P.warm + u));
   for (long long b = 0; b < P.len; b += kU) {
     S xs[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) xs[u] = static_cast<S>(ext(x, n, boundary, P.warm + b + u));
+    for (int u = 0; u < kU; ++u) xs[u] = nx[u];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) nx[u] = static_cast<S>(ext(x, n, boundary, P.warm + b + kU + u));
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       if (b + u >= P.len) break;
