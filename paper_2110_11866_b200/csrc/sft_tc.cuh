@@ -469,27 +469,19 @@ __global__ void __launch_bounds__(kThreads, 1) sft_tc_kernel(const __grid_consta
       if (lane == 0) trace_ev(P, gt, 1);
       const uint32_t d = tmem + (b ? kTD1 : kTD0), x = tmem + kTX + 128 * b;
       if (!warm) {
-        // the pending state GEMM slots in between k-steps as soon as its states are ready
-        // (issue blocks on the tensor pipe's queue: a whole merged GEMM takes ~1000 cycles)
-        auto poll = [&]() {
-          if (pend >= 0 && umma::mbar_test(&M.sready[u & 1], static_cast<uint32_t>((u >> 1) & 1))) {
-            state_gemm();
-            if (lane == 0) trace_ev(P, gt - 1, 5);
-          }
-        };
+        // the whole merged GEMM goes in first; the pending state GEMM follows it (below).
+        // Slotting the state GEMM in between k-steps as soon as its states were ready
+        // measured 2-4% slower (configs 4 and 5, same box): it delays this tile's
+        // aggregates, which start the next scan
         if (P.dbg & 32) {
           merged_hh<0>(dbase, d, x, idm);
           merged_hh<1>(dbase, d, x, idm);
-          poll();
           merged_hh<2>(dbase, d, x, idm);
           merged_hh<3>(dbase, d, x, idm);
         } else {
           merged_k<0>(dbase, d, x, idm);
-          poll();
           merged_k<1>(dbase, d, x, idm);
-          poll();
           merged_k<2>(dbase, d, x, idm);
-          poll();
           merged_k<3>(dbase, d, x, idm);
         }
       } else if (NO == 64) {
