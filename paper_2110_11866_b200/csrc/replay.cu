@@ -16,6 +16,7 @@
 // double for Double, as in the reference's dispatch.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -56,49 +57,65 @@ __device__ __forceinline__ double ext(const double* x, long long n, int boundary
   return m < 0 ? x[0] : x[n - 1];
 }
 
-// pass 1: one thread per order (proj/src/engine.cpp:88-105)
-template <typename S>
+// pass 1: one thread per order (proj/src/engine.cpp:88-105); the strategy is a template
+// parameter so the serial loop carries no branch
+template <typename S, int ST>
 __global__ void recursive_chain_kernel(const RcParams<S>* ps, int n_orders, const double* x, long long n,
                                        int boundary) {
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= n_orders) return;
   const RcParams<S> P = ps[o];
   S v1r = 0, v1i = 0, v2r = 0, v2i = 0, px = 0;
-  // samples are loaded one batch ahead of the dependent chain (software pipeline), so
-  // their latency hides behind the previous batch's kU serial steps
+  auto step = [&](S xm, S& outr, S& outi) {
+    S vr, vi;
+    if constexpr (ST == SFTGPU_RECURSIVE1) {
+      // (zr v1r - zi v1i) + x,  zr v1i + zi v1r
+      vr = add_rn(sub_rn(mul_rn(P.zr, v1r), mul_rn(P.zi, v1i)), xm);
+      vi = add_rn(mul_rn(P.zr, v1i), mul_rn(P.zi, v1r));
+    } else {
+      // ((2c v1r - d v2r) + x) - zcr px,  (2c v1i - d v2i) - zci px
+      vr = sub_rn(add_rn(sub_rn(mul_rn(P.two_cos, v1r), mul_rn(P.dsq, v2r)), xm), mul_rn(P.zcr, px));
+      vi = sub_rn(sub_rn(mul_rn(P.two_cos, v1i), mul_rn(P.dsq, v2i)), mul_rn(P.zci, px));
+    }
+    v2r = v1r;
+    v2i = v1i;
+    v1r = vr;
+    v1i = vi;
+    px = xm;
+    outr = vr;
+    outi = vi;
+  };
+  // samples are loaded two batches ahead of the dependent chain (software pipeline), so
+  // their latency hides behind 2 kU serial steps; full batches have no
+  // bounds checks (the arrays stay in registers), the tail runs step by step
   constexpr int kU = 16;
-  S nx[kU];
+  const long long full = P.len / kU * kU;
+  S nx[kU], nx2[kU];  // batches b + 1 and b + 2 in flight
 #pragma unroll
   for (int u = 0; u < kU; ++u) nx[u] = static_cast<S>(ext(x, n, boundary, P.warm + u));
-  for (long long b = 0; b < P.len; b += kU) {
+#pragma unroll
+  for (int u = 0; u < kU; ++u) nx2[u] = static_cast<S>(ext(x, n, boundary, P.warm + kU + u));
+  long long b = 0;
+  for (; b < full; b += kU) {
     S xs[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) xs[u] = nx[u];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) nx[u] = static_cast<S>(ext(x, n, boundary, P.warm + b + kU + u));
-#pragma unroll
     for (int u = 0; u < kU; ++u) {
-      if (b + u >= P.len) break;
-      const S xm = xs[u];
-      S vr, vi;
-      if (P.strategy == SFTGPU_RECURSIVE1) {
-        // (zr v1r - zi v1i) + x,  zr v1i + zi v1r
-        vr = add_rn(sub_rn(mul_rn(P.zr, v1r), mul_rn(P.zi, v1i)), xm);
-        vi = add_rn(mul_rn(P.zr, v1i), mul_rn(P.zi, v1r));
-      } else {
-        // ((2c v1r - d v2r) + x) - zcr px,  (2c v1i - d v2i) - zci px
-        vr = sub_rn(add_rn(sub_rn(mul_rn(P.two_cos, v1r), mul_rn(P.dsq, v2r)), xm), mul_rn(P.zcr, px));
-        vi = sub_rn(sub_rn(mul_rn(P.two_cos, v1i), mul_rn(P.dsq, v2i)), mul_rn(P.zci, px));
-      }
-      v2r = v1r;
-      v2i = v1i;
-      v1r = vr;
-      v1i = vi;
-      px = xm;
-      P.v[2 * (b + u)] = vr;
-      P.v[2 * (b + u) + 1] = vi;
+      xs[u] = nx[u];
+      nx[u] = nx2[u];
     }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) nx2[u] = static_cast<S>(ext(x, n, boundary, P.warm + b + 2 * kU + u));
+    S vs[2 * kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) step(xs[u], vs[2 * u], vs[2 * u + 1]);
+    // the batch's states leave in 16-byte stores (the plan's state buffer is 256-B aligned
+    // and kU * 2 * sizeof(S) is a multiple of 16)
+    uint4* dst = reinterpret_cast<uint4*>(P.v + 2 * b);
+#pragma unroll
+    for (int i = 0; i < static_cast<int>(2 * kU * sizeof(S) / 16); ++i)
+      dst[i] = *reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(vs) + 16 * i);
   }
+  for (; b < P.len; ++b) step(static_cast<S>(ext(x, n, boundary, P.warm + b)), P.v[2 * b], P.v[2 * b + 1]);
 }
 
 // pass 2: outputs n in [lo, hi] (proj/src/engine.cpp:107-117, sink :33-45)
@@ -189,7 +206,10 @@ cudaError_t run(const sftgpu_config* cfgs, const std::vector<int>& idx, const do
   if (idx.empty()) return cudaSuccess;
   const long long count = hi - lo + 1;
   std::vector<RcParams<S>> ps;
-  for (int i : idx) {
+  std::vector<int> order(idx);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return cfgs[a].strategy == SFTGPU_RECURSIVE1 && cfgs[b].strategy != SFTGPU_RECURSIVE1; });
+  for (int i : order) {
     RcParams<S> P = host_params<S>(cfgs[i]);
     P.warm = lo - P.K - (2 * P.K + 1);
     P.len = hi + P.K - P.warm + 1;
@@ -206,7 +226,12 @@ cudaError_t run(const sftgpu_config* cfgs, const std::vector<int>& idx, const do
   if ((e = cudaMemcpy(dps, ps.data(), ps.size() * sizeof(RcParams<S>), cudaMemcpyHostToDevice)) != cudaSuccess)
     return e;
   const int no = static_cast<int>(ps.size());
-  recursive_chain_kernel<S><<<(no + 31) / 32, 32>>>(dps, no, dx, n, boundary);
+  // one thread per order (ps is sorted by strategy): one launch per strategy
+  const int n1 = static_cast<int>(std::count_if(ps.begin(), ps.end(),
+                                                [](const RcParams<S>& q) { return q.strategy == SFTGPU_RECURSIVE1; }));
+  if (n1 > 0) recursive_chain_kernel<S, SFTGPU_RECURSIVE1><<<(n1 + 31) / 32, 32>>>(dps, n1, dx, n, boundary);
+  if (no > n1)
+    recursive_chain_kernel<S, SFTGPU_RECURSIVE2><<<(no - n1 + 31) / 32, 32>>>(dps + n1, no - n1, dx, n, boundary);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   for (int j = 0; j < no; ++j) {
     const long long blocks = std::min<long long>((count + 255) / 256, 4096);
