@@ -165,14 +165,15 @@ ComponentSeq run_components(const Signal& sig, const SftConfig& cfg, std::int64_
   return ComponentSeq{ArrayXd(c.begin(), c.end()), ArrayXd(s.begin(), s.end())};
 }
 // Recursive1/2 (engine.cpp:53-120) replayed on the GPU with the reference's rounding (K7)
-inline ComponentSeq replay(const Signal& sig, const SftConfig& cfg, std::int64_t lo, std::int64_t hi, int mode) {
+inline ComponentSeq replay(const Signal& sig, const SftConfig& cfg, std::int64_t lo, std::int64_t hi, int mode,
+                           double* max_state = nullptr) {
   if (mode == 1 && cfg.alpha != 0.0) throw std::invalid_argument("sft_components: alpha must be 0 (use asft_components)");
   if (mode == 2 && !(cfg.alpha > 0.0)) throw std::invalid_argument("asft_components: alpha must be > 0");
   const sftgpu_config rc = cfg.raw();
   const size_t cnt = hi >= lo ? static_cast<size_t>(hi - lo + 1) : 1;
   ComponentSeq out{ArrayXd(cnt), ArrayXd(cnt)};
   check(sftgpu_components_replay(&rc, 1, sig.samples.data(), sig.size(), static_cast<int>(sig.boundary), lo, hi,
-                                 out.c.data(), out.s.data()));
+                                 out.c.data(), out.s.data(), max_state));
   return out;
 }
 inline ComponentSeq components(const Signal& sig, const SftConfig& cfg, std::int64_t lo, std::int64_t hi, int mode) {
@@ -245,7 +246,11 @@ inline StabilityReport stability_probe(const Signal& sig, const SftConfig& cfg) 
   SftConfig sc = cfg, dc = cfg;
   sc.precision = Precision::Single;
   dc.precision = Precision::Double;
-  const ComponentSeq lo = components_over(sig, sc, 0, sig.size() - 1);
+  // recursive strategies: the reference's own fp32 recurrence and its peak filter state
+  const bool rec = cfg.strategy != Strategy::KernelIntegral && cfg.order.integer_order;
+  double peak = 0.0;
+  const ComponentSeq lo = rec ? detail::replay(sig, sc, 0, sig.size() - 1, 0, &peak)
+                              : components_over(sig, sc, 0, sig.size() - 1);
   const ComponentSeq ref = components_over(sig, dc, 0, sig.size() - 1);
   StabilityReport r;
   r.abs_error.resize(ref.c.size());
@@ -254,8 +259,9 @@ inline StabilityReport stability_probe(const Signal& sig, const SftConfig& cfg) 
     r.abs_error[n] = std::max(std::abs(lo.c[n] - ref.c[n]), std::abs(lo.s[n] - ref.s[n]));
     emax = std::max(emax, r.abs_error[n]);
     r.reference_scale = std::max({r.reference_scale, std::abs(ref.c[n]), std::abs(ref.s[n])});
-    r.max_state_magnitude = std::max(r.max_state_magnitude, std::hypot(lo.c[n], lo.s[n]));
+    if (!rec) r.max_state_magnitude = std::max(r.max_state_magnitude, std::hypot(lo.c[n], lo.s[n]));
   }
+  if (rec) r.max_state_magnitude = peak;
   r.max_component_error = r.reference_scale > 0.0 ? emax / r.reference_scale : emax;
   return r;
 }

@@ -354,9 +354,13 @@ int sftgpu_sft_via_sliding_sum(const sftgpu_config* cfg, const double* x_host, i
  * strategy through sftgpu_components_plan_create) is the fast path and the more accurate
  * one; this entry is for callers who need the reference's numbers exactly.
  * cfgs: n_orders configs with strategy SFTGPU_RECURSIVE1/2 (any K / alpha / precision mix);
- * HOST fp64 signal in; c = Re, s = -Im out, [n_orders][hi - lo + 1]; synchronous. */
+ * HOST fp64 signal in; c = Re, s = -Im out, [n_orders][hi - lo + 1]; max_state (NULL or
+ * [n_orders]) = the peak |filter state| over the chain, the quantity stability_probe
+ * reports (src/engine.cpp:101, :304-312; |.| by hypot in the Scalar precision, which may
+ * differ from the host libm's in the last bit); synchronous. */
 int sftgpu_components_replay(const sftgpu_config* cfgs, int n_orders, const double* x_host, int64_t n,
-                             int boundary, int64_t lo, int64_t hi, double* c_host, double* s_host);
+                             int boundary, int64_t lo, int64_t hi, double* c_host, double* s_host,
+                             double* max_state);
 
 /* Host-memory variants (device buffers managed internally; synchronous). */
 int sftgpu_sliding_sum_host(int dtype, int blocked, const void* f_host, int64_t n, int64_t L, void* out_host);

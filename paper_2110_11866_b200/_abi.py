@@ -152,8 +152,8 @@ SIGNATURES = {
                           C.POINTER(C.c_double)], _I),
     "sftgpu_reconstruct": ([C.POINTER(Coeffs), C.c_void_p, _I64, C.c_void_p], _I),
     "sftgpu_sft_via_sliding_sum": ([C.POINTER(Config), C.c_void_p, _I64, _I, C.c_void_p, C.c_void_p], _I),
-    "sftgpu_components_replay": ([C.POINTER(Config), _I, C.c_void_p, _I64, _I, _I64, _I64, C.c_void_p, C.c_void_p],
-                                 _I),
+    "sftgpu_components_replay": ([C.POINTER(Config), _I, C.c_void_p, _I64, _I, _I64, _I64, C.c_void_p, C.c_void_p,
+                                  C.c_void_p], _I),
     "sftgpu_generate_signal": ([_I, _I64, _U64, _I64, _I, _P, _P], _I),
     "sftgpu_truncated_convolution": ([_P, _I64, _I, _P, _I64, _I64, _P, _P], _I),
 }

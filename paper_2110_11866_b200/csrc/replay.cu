@@ -39,6 +39,7 @@ struct RcParams {
   int window_2k1;
   long long K, warm, len;  // chain positions warm .. warm + len - 1
   S* v;              // [len] complex states (interleaved)
+  double* peak;      // max |v| over the chain (the reference's max_state, engine.cpp:101)
   double* c;         // [count]
   double* s;
 };
@@ -49,6 +50,10 @@ __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, 
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+// |v| of a complex<Scalar> (std::abs: hypot in the Scalar's precision)
+__device__ __forceinline__ float hypot_of(float a, float b) { return hypotf(a, b); }
+__device__ __forceinline__ double hypot_of(double a, double b) { return hypot(a, b); }
 
 // extended_sample (proj/include/sft/signal.hpp:35-45)
 __device__ __forceinline__ double ext(const double* x, long long n, int boundary, long long m) {
@@ -66,6 +71,7 @@ __global__ void recursive_chain_kernel(const RcParams<S>* ps, int n_orders, cons
   if (o >= n_orders) return;
   const RcParams<S> P = ps[o];
   S v1r = 0, v1i = 0, v2r = 0, v2i = 0, px = 0;
+  double pk = 0.0;
   auto step = [&](S xm, S& outr, S& outi) {
     S vr, vi;
     if constexpr (ST == SFTGPU_RECURSIVE1) {
@@ -84,6 +90,7 @@ __global__ void recursive_chain_kernel(const RcParams<S>* ps, int n_orders, cons
     px = xm;
     outr = vr;
     outi = vi;
+    pk = fmax(pk, static_cast<double>(hypot_of(vr, vi)));
   };
   // samples are loaded two batches ahead of the dependent chain (software pipeline), so
   // their latency hides behind 2 kU serial steps; full batches have no
@@ -116,6 +123,7 @@ __global__ void recursive_chain_kernel(const RcParams<S>* ps, int n_orders, cons
       dst[i] = *reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(vs) + 16 * i);
   }
   for (; b < P.len; ++b) step(static_cast<S>(ext(x, n, boundary, P.warm + b)), P.v[2 * b], P.v[2 * b + 1]);
+  *P.peak = pk;
 }
 
 // pass 2: outputs n in [lo, hi] (proj/src/engine.cpp:107-117, sink :33-45)
@@ -202,7 +210,7 @@ struct DevBufs {
 
 template <typename S>
 cudaError_t run(const sftgpu_config* cfgs, const std::vector<int>& idx, const double* dx, long long n, int boundary,
-                long long lo, long long hi, double* dc, double* ds, DevBufs& bufs) {
+                long long lo, long long hi, double* dc, double* ds, double* dpeak, DevBufs& bufs) {
   if (idx.empty()) return cudaSuccess;
   const long long count = hi - lo + 1;
   std::vector<RcParams<S>> ps;
@@ -217,6 +225,7 @@ cudaError_t run(const sftgpu_config* cfgs, const std::vector<int>& idx, const do
     if (e != cudaSuccess) return e;
     P.c = dc + static_cast<long long>(i) * count;
     P.s = ds + static_cast<long long>(i) * count;
+    P.peak = dpeak + i;
     ps.push_back(P);
   }
   // pass 2 writes c/s of order o at o * count: give each its own base (o = 0 per entry)
@@ -244,7 +253,8 @@ cudaError_t run(const sftgpu_config* cfgs, const std::vector<int>& idx, const do
 }  // namespace
 
 extern "C" int sftgpu_components_replay(const sftgpu_config* cfgs, int n_orders, const double* x_host, int64_t n,
-                                        int boundary, int64_t lo, int64_t hi, double* c_host, double* s_host) {
+                                        int boundary, int64_t lo, int64_t hi, double* c_host, double* s_host,
+                                        double* max_state) {
   auto bad = [](const char* m) {
     sftgpu_set_error(m);
     return SFTGPU_EINVAL;
@@ -274,16 +284,19 @@ extern "C" int sftgpu_components_replay(const sftgpu_config* cfgs, int n_orders,
   std::vector<int> f32, f64;
   for (int i = 0; i < n_orders; ++i) (cfgs[i].precision == SFTGPU_SINGLE ? f32 : f64).push_back(i);
   DevBufs bufs;
-  double *dx = nullptr, *dc = nullptr, *ds = nullptr;
+  double *dx = nullptr, *dc = nullptr, *ds = nullptr, *dpeak = nullptr;
   const size_t out_bytes = static_cast<size_t>(n_orders) * count * sizeof(double);
   cudaError_t e = bufs.alloc(&dx, n * sizeof(double));
   if (e == cudaSuccess) e = bufs.alloc(&dc, out_bytes);
   if (e == cudaSuccess) e = bufs.alloc(&ds, out_bytes);
+  if (e == cudaSuccess) e = bufs.alloc(&dpeak, static_cast<size_t>(n_orders) * sizeof(double));
   if (e == cudaSuccess) e = cudaMemcpy(dx, x_host, n * sizeof(double), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = run<float>(cfgs, f32, dx, n, boundary, lo, hi, dc, ds, bufs);
-  if (e == cudaSuccess) e = run<double>(cfgs, f64, dx, n, boundary, lo, hi, dc, ds, bufs);
+  if (e == cudaSuccess) e = run<float>(cfgs, f32, dx, n, boundary, lo, hi, dc, ds, dpeak, bufs);
+  if (e == cudaSuccess) e = run<double>(cfgs, f64, dx, n, boundary, lo, hi, dc, ds, dpeak, bufs);
   if (e == cudaSuccess) e = cudaMemcpy(c_host, dc, out_bytes, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess) e = cudaMemcpy(s_host, ds, out_bytes, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && max_state)
+    e = cudaMemcpy(max_state, dpeak, static_cast<size_t>(n_orders) * sizeof(double), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) {
     sftgpu_set_error(std::string("components_replay: ") + cudaGetErrorString(e));
     return SFTGPU_ECUDA;

@@ -223,10 +223,11 @@ def _components(sig: Signal, cfgs, lo: int, hi: int, mode: int):
     return c.double().cpu().numpy(), s.double().cpu().numpy()
 
 
-def components_replay(sig: Signal, cfgs, lo: int, hi: int):
+def components_replay(sig: Signal, cfgs, lo: int, hi: int, want_state: bool = False):
     """proj/src/engine.cpp:53-120 (recursive_components): Recursive1 / Recursive2 replayed on
     the GPU with the reference's own operation order (K7, ``sftgpu_components_replay``), so
-    the result is bit-identical to the reference's. (c, s) as [n_cfgs][hi - lo + 1]."""
+    the result is bit-identical to the reference's. (c, s) as [n_cfgs][hi - lo + 1], plus
+    the per-config peak |filter state| (engine.cpp:101) with ``want_state``."""
     cfgs = list(cfgs)
     n = sig.size()
     count = hi - lo + 1 if hi >= lo else 0
@@ -234,9 +235,11 @@ def components_replay(sig: Signal, cfgs, lo: int, hi: int):
     c = np.empty((len(cfgs), max(count, 1)), dtype=np.float64)
     s = np.empty_like(c)
     arr = (_abi.Config * len(cfgs))(*[cf._c() for cf in cfgs])
+    peak = np.zeros(len(cfgs), dtype=np.float64)
     check(lib().sftgpu_components_replay(arr, len(cfgs), x.ctypes.data_as(C.c_void_p), n, int(sig.boundary), lo, hi,
-                                         c.ctypes.data_as(C.c_void_p), s.ctypes.data_as(C.c_void_p)))
-    return c, s
+                                         c.ctypes.data_as(C.c_void_p), s.ctypes.data_as(C.c_void_p),
+                                         peak.ctypes.data_as(C.c_void_p)))
+    return (c, s, peak) if want_state else (c, s)
 
 
 def _one(sig: Signal, cfg: SftConfig, lo: int, hi: int, mode: int, exact: bool) -> ComponentSeq:
@@ -620,16 +623,24 @@ class StabilityReport:  # include/sft/engine.hpp:94-100
 
 def stability_probe(sig: Signal, cfg: SftConfig) -> StabilityReport:
     """proj/src/engine.cpp:302-320: cfg at single precision against double (both GPU).
-    max_state_magnitude is the peak |window state| of the fp32 scan."""
+    max_state_magnitude: the peak |filter state| of the single-precision recurrence for the
+    recursive strategies (K7, as the reference), else the peak |window state| of the scan."""
     n = sig.size()
     mk = lambda p: SftConfig(cfg.half_width, cfg.beta, cfg.order, cfg.alpha, cfg.n0, cfg.strategy, p,  # noqa: E731
                              cfg.window_2k1)
-    lo = components_over(sig, mk(Precision.Single), 0, n - 1)
+    if cfg.strategy != Strategy.KernelIntegral and cfg.order.integer_order:
+        # recursive strategies: the reference's own single-precision recurrence (K7) and
+        # its peak filter-state magnitude
+        c, s, peak = components_replay(sig, [mk(Precision.Single)], 0, n - 1, want_state=True)
+        lo = ComponentSeq(c[0], s[0])
+        max_state = float(peak[0])
+    else:
+        lo = components_over(sig, mk(Precision.Single), 0, n - 1)
+        max_state = float(np.hypot(lo.c, lo.s).max())
     ref = components_over(sig, mk(Precision.Double), 0, n - 1)
     err = np.maximum(np.abs(lo.c - ref.c), np.abs(lo.s - ref.s))
     scale = float(max(np.abs(ref.c).max(), np.abs(ref.s).max()))
-    return StabilityReport(float(np.hypot(lo.c, lo.s).max()), float(err.max() / scale if scale > 0 else err.max()),
-                           scale, err)
+    return StabilityReport(max_state, float(err.max() / scale if scale > 0 else err.max()), scale, err)
 
 
 @dataclass

@@ -119,3 +119,21 @@ def test_replay_errors(sft):
         sft.components_replay(x, [_cfg(sft, 4, math.pi / 4, 1, 0.0, 0, 1)], 0, 31)
     with pytest.raises(ValueError, match="K must be >= 1"):
         sft.components_replay(x, [_cfg(sft, 0, math.pi / 4, 1, 0.0, 2, 1)], 0, 31)
+
+
+def test_replay_peak_state_and_stability_probe(sft, O):
+    """stability_probe on a recursive strategy reports the reference's max_state (the peak
+    |filter state| of the fp32 recurrence, engine.cpp:101) and honours the bound of
+    proj/tests/test_engine.cpp:305-317."""
+    sigma = 32.0
+    alpha = 2.0 * (1.0 / (2.0 * sigma * sigma)) * 4.0
+    K = int(3 * sigma)
+    x = O.make_test_signal(O.SEEDED_NOISE, 4000, 3)
+    cf = _cfg(sft, K, math.pi / K, 2, alpha, 1, 0)
+    rep = sft.stability_probe(sft.Signal(x), cf)
+    bound = np.max(np.abs(x)) / (1.0 - math.exp(-alpha))
+    assert rep.max_state_magnitude <= bound
+    assert rep.max_component_error < 1e-2
+    _, _, ms = O.components_over(x, 1, O.Cfg(K, math.pi / K, 2, alpha=alpha, strategy=1, precision=0), 0, 3999,
+                                 want_state=True)
+    assert abs(rep.max_state_magnitude - ms) <= 1e-6 * ms
