@@ -356,8 +356,8 @@ int sftgpu_sft_via_sliding_sum(const sftgpu_config* cfg, const double* x_host, i
  * cfgs: n_orders configs with strategy SFTGPU_RECURSIVE1/2 (any K / alpha / precision mix);
  * HOST fp64 signal in; c = Re, s = -Im out, [n_orders][hi - lo + 1]; max_state (NULL or
  * [n_orders]) = the peak |filter state| over the chain, the quantity stability_probe
- * reports (src/engine.cpp:101, :304-312; |.| by hypot in the Scalar precision, which may
- * differ from the host libm's in the last bit); synchronous. */
+ * reports (src/engine.cpp:101, :304-312; the root of the peak |v|^2 in fp64, which may
+ * differ from the reference's hypot in the Scalar precision in the last bits); synchronous. */
 int sftgpu_components_replay(const sftgpu_config* cfgs, int n_orders, const double* x_host, int64_t n,
                              int boundary, int64_t lo, int64_t hi, double* c_host, double* s_host,
                              double* max_state);

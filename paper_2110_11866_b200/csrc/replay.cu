@@ -51,10 +51,6 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
 
-// |v| of a complex<Scalar> (std::abs: hypot in the Scalar's precision)
-__device__ __forceinline__ float hypot_of(float a, float b) { return hypotf(a, b); }
-__device__ __forceinline__ double hypot_of(double a, double b) { return hypot(a, b); }
-
 // extended_sample (proj/include/sft/signal.hpp:35-45)
 __device__ __forceinline__ double ext(const double* x, long long n, int boundary, long long m) {
   if (m >= 0 && m < n) return x[m];
@@ -72,7 +68,7 @@ __global__ void recursive_chain_kernel(const RcParams<S>* ps, int n_orders, cons
   const RcParams<S> P = ps[o];
   S v1r = 0, v1i = 0, v2r = 0, v2i = 0, px = 0;
   double pk = 0.0;
-  auto step = [&](S xm, S& outr, S& outi) {
+  auto step = [&](S xm, S& outr, S& outi, double& m2) {
     S vr, vi;
     if constexpr (ST == SFTGPU_RECURSIVE1) {
       // (zr v1r - zi v1i) + x,  zr v1i + zi v1r
@@ -90,7 +86,8 @@ __global__ void recursive_chain_kernel(const RcParams<S>* ps, int n_orders, cons
     px = xm;
     outr = vr;
     outi = vi;
-    pk = fmax(pk, static_cast<double>(hypot_of(vr, vi)));
+    // |v|^2 in fp64, off the chain (reduced per batch; the root is taken once at the end)
+    m2 = fma(static_cast<double>(vr), static_cast<double>(vr), static_cast<double>(vi) * vi);
   };
   // samples are loaded two batches ahead of the dependent chain (software pipeline), so
   // their latency hides behind 2 kU serial steps; full batches have no
@@ -113,8 +110,14 @@ __global__ void recursive_chain_kernel(const RcParams<S>* ps, int n_orders, cons
 #pragma unroll
     for (int u = 0; u < kU; ++u) nx2[u] = static_cast<S>(ext(x, n, boundary, P.warm + b + 2 * kU + u));
     S vs[2 * kU];
+    double m2[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) step(xs[u], vs[2 * u], vs[2 * u + 1]);
+    for (int u = 0; u < kU; ++u) step(xs[u], vs[2 * u], vs[2 * u + 1], m2[u]);
+#pragma unroll
+    for (int w = kU / 2; w >= 1; w >>= 1)
+#pragma unroll
+      for (int u = 0; u < w; ++u) m2[u] = fmax(m2[u], m2[u + w]);
+    pk = fmax(pk, m2[0]);
     // the batch's states leave in 16-byte stores (the plan's state buffer is 256-B aligned
     // and kU * 2 * sizeof(S) is a multiple of 16)
     uint4* dst = reinterpret_cast<uint4*>(P.v + 2 * b);
@@ -122,8 +125,12 @@ __global__ void recursive_chain_kernel(const RcParams<S>* ps, int n_orders, cons
     for (int i = 0; i < static_cast<int>(2 * kU * sizeof(S) / 16); ++i)
       dst[i] = *reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(vs) + 16 * i);
   }
-  for (; b < P.len; ++b) step(static_cast<S>(ext(x, n, boundary, P.warm + b)), P.v[2 * b], P.v[2 * b + 1]);
-  *P.peak = pk;
+  for (; b < P.len; ++b) {
+    double m2;
+    step(static_cast<S>(ext(x, n, boundary, P.warm + b)), P.v[2 * b], P.v[2 * b + 1], m2);
+    pk = fmax(pk, m2);
+  }
+  *P.peak = sqrt(pk);
 }
 
 // pass 2: outputs n in [lo, hi] (proj/src/engine.cpp:107-117, sink :33-45)
